@@ -1,0 +1,137 @@
+/*
+ * kp_abi.h -- C-ABI of the B200 kernel library (libkp.so).
+ *
+ * This is the drop-in boundary between the reference's Python host API
+ * (kernelprune: dataset / pruning / selector / codegen, reference
+ * pkg/src/kernelprune/) and the sm_100a kernels.  Plain C: no CUDA or torch
+ * types appear in any signature; device pointers are `void*`/`float*`, the
+ * CUDA stream is an opaque `void*` (a cudaStream_t, NULL = legacy default).
+ *
+ * Reference interfaces replaced (file:line under /root/reference):
+ *   kp_config                 <- KernelConfig, pkg/src/kernelprune/dataset.py:63-86
+ *                                (field order == canonical order), and the
+ *                                generated `<sym>_config` struct, codegen.py:138-144
+ *   kp_num_configs/config_at  <- all_configs(), dataset.py:119-126 (640 configs,
+ *                                canonical lexicographic order)
+ *   kp_config_valid           <- KernelConfig.__post_init__, dataset.py:77-83
+ *                                (InvalidConfigValue -> KP_ERR_INVALID_CONFIG)
+ *   kp_gemm                   <- the paper's "matmul kernel with a tile config"
+ *                                (PAPER.md:116-125); geometry as pinned by
+ *                                synthetic.analytic_perf, synthetic.py:65-70
+ *   kp_gemm_time              <- per-cell "run config on problem -> runtime_ns",
+ *                                the measured twin of synthetic.generate,
+ *                                synthetic.py:92-114 (runtime_ns = 2mnk/gflops)
+ *   kp_sweep_problem          <- the inner loop of generate() over all configs
+ *                                of one problem, synthetic.py:106-113
+ *   kp_select / kp_gemm_auto  <- generated `select_kernel(m,k,n)`,
+ *                                codegen.py:128-171, compiled into the library
+ *                                exactly as harness/parity_main.cpp:21-32,96 does
+ *   kp_status                 <- errors.py:4-9 DataError taxonomy; NonPositiveValue
+ *                                (dataset.py:95-97) -> KP_ERR_BAD_SHAPE
+ *
+ * Conventions: every entry point returns a status and never aborts; the
+ * library allocates no device memory per call (TMEM is allocated/freed inside
+ * the tcgen05 kernels); calls are stream-ordered and reentrant; the message of
+ * the last failure on the calling thread is available from kp_last_error().
+ */
+#ifndef KP_ABI_H
+#define KP_ABI_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KP_ABI_VERSION 1
+
+/* Same layout as KernelConfig / the generated select_kernel_config struct. */
+typedef struct {
+    uint32_t acc;       /* K step per register fragment: 1,2,4,8          */
+    uint32_t row_tile;  /* output rows per thread: 1,2,4,8                */
+    uint32_t col_tile;  /* output cols per thread: 1,2,4,8                */
+    uint32_t wg_rows;   /* work-group shape (runtime launch parameter)    */
+    uint32_t wg_cols;
+} kp_config;
+
+typedef enum {
+    KP_F32_SIMT = 0,  /* fp32 in, FFMA register-tiled, fp32 out          */
+    KP_TF32_TC  = 1,  /* fp32 in (rounded to tf32), tcgen05 kind::tf32   */
+    KP_BF16_TC  = 2   /* bf16 in, tcgen05 kind::f16, fp32 accumulate/out */
+} kp_family;
+
+typedef enum {
+    KP_OK = 0,
+    KP_ERR_INVALID_CONFIG = 1,  /* config outside the family's domain      */
+    KP_ERR_BAD_SHAPE = 2,       /* m,k,n,batch < 1 or ld too small          */
+    KP_ERR_ALIGNMENT = 3,       /* pointer/ld alignment the family requires */
+    KP_ERR_UNSUPPORTED = 4,     /* family/variant not built or no device    */
+    KP_ERR_CUDA = 5,            /* a CUDA runtime call failed               */
+    KP_ERR_INVALID_ARG = 6      /* null pointer, bad counts                 */
+} kp_status;
+
+/*
+ * One (optionally strided-batched) GEMM, row-major like numpy:
+ *   C[b] = alpha * op(A[b]) @ op(B[b]) + beta * C[b],   b in [0, batch)
+ * op(A) is m x k: trans_a == 0 -> A[b][i*lda + p], else A[b][p*lda + i].
+ * op(B) is k x n: trans_b == 0 -> B[b][p*ldb + j], else B[b][j*ldb + p].
+ * C is m x n: C[b][i*ldc + j].  Strides are in elements.  beta == 0 means C
+ * is write-only (never read).
+ */
+typedef struct {
+    int64_t batch, m, k, n;
+    int32_t trans_a, trans_b;
+    int64_t lda, ldb, ldc;
+    int64_t stride_a, stride_b, stride_c;
+    float alpha, beta;
+} kp_gemm_desc;
+
+/* ---- config space (canonical order = KernelConfig sort order) -------- */
+int32_t   kp_abi_version(void);
+int32_t   kp_num_configs(kp_family family);
+kp_status kp_config_at(kp_family family, int32_t index, kp_config* out);
+kp_status kp_config_valid(kp_family family, kp_config cfg);
+
+/* ---- compute ----------------------------------------------------------- */
+kp_status kp_gemm(kp_family family, kp_config cfg, const kp_gemm_desc* desc,
+                  const void* A, const void* B, float* C, void* stream);
+
+/* Warm up, then time `reps` samples of back-to-back launches (each sample
+ * >= min_sample_ns of device time, launch count per sample chosen from the
+ * warm-up); *runtime_ns = median per-launch device time (CUDA events on
+ * `stream`).  Synchronises `stream`. */
+kp_status kp_gemm_time(kp_family family, kp_config cfg, const kp_gemm_desc* desc,
+                       const void* A, const void* B, float* C,
+                       int32_t warmup, int32_t reps, double min_sample_ns,
+                       double* runtime_ns, void* stream);
+
+/* Time every config in `cfgs` on one problem (buffers allocated once by the
+ * caller); runtime_ns[i] per config, same timing method as kp_gemm_time. */
+kp_status kp_sweep_problem(kp_family family, const kp_config* cfgs, int32_t n_cfgs,
+                           const kp_gemm_desc* desc, const void* A, const void* B,
+                           float* C, int32_t warmup, int32_t reps,
+                           double min_sample_ns, double* runtime_ns, void* stream);
+
+/* ---- runtime selection (generated decision-tree header) --------------- */
+/* Config the compiled selector picks for (m,k,n); KP_ERR_UNSUPPORTED when no
+ * selector is compiled in for this family / transpose variant. */
+kp_status kp_select(kp_family family, int32_t trans_a, int32_t trans_b,
+                    int64_t m, int64_t k, int64_t n, kp_config* out);
+kp_status kp_gemm_auto(kp_family family, const kp_gemm_desc* desc,
+                       const void* A, const void* B, float* C, void* stream,
+                       kp_config* chosen /* may be NULL */);
+
+/* ---- diagnostics -------------------------------------------------------- */
+const char* kp_status_string(kp_status status);
+const char* kp_last_error(void);               /* thread-local */
+/* Number of kernel launches this process issued through the library. */
+int64_t     kp_launch_count(void);
+/* Device facts for the sweep sidecar: SM count, max SM clock (kHz),
+ * compute capability (major*10+minor). */
+kp_status   kp_device_info(int32_t device, int32_t* sm_count, int32_t* sm_clock_khz,
+                           int32_t* cc);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KP_ABI_H */

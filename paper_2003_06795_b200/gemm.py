@@ -1,0 +1,193 @@
+"""Matmul-with-config: the Python face of the kernel families.
+
+This is the call north_star asks for beside the reference's config ->
+performance function (synthetic.analytic_perf, reference
+pkg/src/kernelprune/synthetic.py:65): run *this* KernelConfig on *this*
+problem, on the B200, through the C-ABI (include/kp_abi.h). PyTorch is used
+only for device memory and the current CUDA stream; the arithmetic is in
+libkp.so. There is no CPU fallback: without the library or a GPU every entry
+point raises.
+
+Operands are logical: ``a`` is op(A) with shape (m, k) or (batch, m, k) and
+``b`` is op(B) with shape (k, n) or (batch, k, n). A transposed view (e.g.
+``x.t()``) is passed to the kernel as a trans_a / trans_b layout without a
+copy; a 2-D operand next to a 3-D one is broadcast with batch stride 0.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native as nat
+from .dataset import KernelConfig
+
+_DTYPE_OF = {}
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _family_dtype(family: int):
+    torch = _torch()
+    return torch.bfloat16 if family == nat.BF16_TC else torch.float32
+
+
+def _operand_layout(t, rows: int, cols: int):
+    """(transposed, ld) for a logical rows x cols operand view, or None."""
+    s_r, s_c = t.stride(-2), t.stride(-1)
+    if s_c == 1 or cols == 1:
+        ld = s_r if rows > 1 else cols
+        if ld >= cols:
+            return False, ld
+    if s_r == 1 or rows == 1:
+        ld = s_c if cols > 1 else rows
+        if ld >= rows:
+            return True, ld
+    return None
+
+
+def _prep(t, rows, cols):
+    lay = _operand_layout(t, rows, cols)
+    if lay is None:
+        t = t.contiguous()
+        lay = (False, cols)
+    return t, lay
+
+
+def describe(a, b, out=None, alpha: float = 1.0, beta: float = 0.0, family="f32"):
+    """Validate operands and build (desc, a, b, out) for the C-ABI."""
+    torch = _torch()
+    fam = nat.family_id(family)
+    want = _family_dtype(fam)
+    if a.dim() not in (2, 3) or b.dim() not in (2, 3):
+        raise nat.BadProblemShape("operands must be 2-D or 3-D (batched)")
+    if a.dtype != want or b.dtype != want:
+        raise nat.BadProblemShape(f"family {family!r} expects {want} operands, "
+                                  f"got {a.dtype} and {b.dtype}")
+    if not (a.is_cuda and b.is_cuda):
+        raise nat.KernelLibraryError("operands must be CUDA tensors (no CPU fallback)")
+    m, k = a.shape[-2], a.shape[-1]
+    k2, n = b.shape[-2], b.shape[-1]
+    if k != k2:
+        raise nat.BadProblemShape(f"inner dims differ: a is {tuple(a.shape)}, b is {tuple(b.shape)}")
+    batch_a = a.shape[0] if a.dim() == 3 else 1
+    batch_b = b.shape[0] if b.dim() == 3 else 1
+    if batch_a != batch_b and 1 not in (batch_a, batch_b):
+        raise nat.BadProblemShape("batch sizes differ")
+    batch = max(batch_a, batch_b)
+    a, (ta, lda) = _prep(a, m, k)
+    b, (tb, ldb) = _prep(b, k, n)
+    sa = a.stride(0) if a.dim() == 3 and batch_a > 1 else 0
+    sb = b.stride(0) if b.dim() == 3 and batch_b > 1 else 0
+    shape = (batch, m, n) if (a.dim() == 3 or b.dim() == 3) else (m, n)
+    if out is None:
+        if beta != 0.0:
+            raise nat.BadProblemShape("beta != 0 needs an `out` tensor")
+        out = torch.empty(shape, dtype=torch.float32, device=a.device)
+    else:
+        if out.dtype != torch.float32 or tuple(out.shape) != shape or out.stride(-1) != 1:
+            raise nat.BadProblemShape(f"out must be float32 {shape} with unit column stride")
+    ldc = out.stride(-2) if m > 1 else n
+    sc = out.stride(0) if out.dim() == 3 else m * ldc
+    desc = nat.KpGemmDesc(batch, m, k, n, int(ta), int(tb), lda, ldb, ldc, sa, sb, sc,
+                          float(alpha), float(beta))
+    return desc, a, b, out
+
+
+def _stream_handle():
+    torch = _torch()
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def matmul(a, b, config=None, *, family="f32", out=None, alpha: float = 1.0,
+           beta: float = 0.0):
+    """C = alpha * a @ b + beta * out on the GPU with one kernel config.
+
+    ``config=None`` uses the runtime selector compiled into the library (the
+    generated decision-tree header, codegen.emit_selector_source).
+    """
+    fam = nat.family_id(family)
+    desc, a, b, out = describe(a, b, out, alpha, beta, family)
+    lib = nat.lib()
+    if config is None:
+        chosen = nat.KpConfig()
+        nat.check(lib.kp_gemm_auto(fam, ctypes.byref(desc), a.data_ptr(), b.data_ptr(),
+                                   out.data_ptr(), _stream_handle(), ctypes.byref(chosen)),
+                  "kp_gemm_auto")
+    else:
+        nat.check(lib.kp_gemm(fam, nat.to_kp_config(config), ctypes.byref(desc), a.data_ptr(),
+                              b.data_ptr(), out.data_ptr(), _stream_handle()), "kp_gemm")
+    return out
+
+
+def matmul_host(a: np.ndarray, b: np.ndarray, config=None, *, family="f32", device=0):
+    """Host-buffer entry point (numpy in, numpy out): pinned H2D copies, the
+    kernel, and the D2H copy, all stream-ordered. Used for the e2e figure."""
+    torch = _torch()
+    fam = nat.family_id(family)
+    want = _family_dtype(fam)
+    ta = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).pin_memory()
+    tb = torch.from_numpy(np.ascontiguousarray(b, dtype=np.float32)).pin_memory()
+    dev = torch.device("cuda", device)
+    da = ta.to(dev, non_blocking=True).to(want)
+    db = tb.to(dev, non_blocking=True).to(want)
+    dc = matmul(da, db, config, family=family)
+    host = torch.empty(dc.shape, dtype=torch.float32, pin_memory=True)
+    host.copy_(dc, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return host.numpy()
+
+
+def time_config(a, b, config, *, family="f32", out=None, warmup: int = 3, reps: int = 10,
+                min_sample_ns: float = 50_000.0) -> float:
+    """Median per-launch device time (ns) of one config on one problem."""
+    fam = nat.family_id(family)
+    desc, a, b, out = describe(a, b, out, 1.0, 0.0, family)
+    res = ctypes.c_double()
+    nat.check(nat.lib().kp_gemm_time(fam, nat.to_kp_config(config), ctypes.byref(desc),
+                                     a.data_ptr(), b.data_ptr(), out.data_ptr(), warmup, reps,
+                                     min_sample_ns, ctypes.byref(res), _stream_handle()),
+              "kp_gemm_time")
+    return res.value
+
+
+def sweep_problem(a, b, configs, *, family="f32", out=None, warmup: int = 2, reps: int = 5,
+                  min_sample_ns: float = 50_000.0) -> list[float]:
+    """Median runtime (ns) of every config on one problem (C++ timing loop)."""
+    fam = nat.family_id(family)
+    desc, a, b, out = describe(a, b, out, 1.0, 0.0, family)
+    cfgs = (nat.KpConfig * len(configs))(*[nat.to_kp_config(c) for c in configs])
+    res = (ctypes.c_double * len(configs))()
+    nat.check(nat.lib().kp_sweep_problem(fam, cfgs, len(configs), ctypes.byref(desc),
+                                         a.data_ptr(), b.data_ptr(), out.data_ptr(), warmup,
+                                         reps, min_sample_ns, res, _stream_handle()),
+              "kp_sweep_problem")
+    return list(res)
+
+
+def family_configs(family="f32") -> tuple[KernelConfig, ...]:
+    """The family's config list in canonical order (kp_config_at)."""
+    fam = nat.family_id(family)
+    lib = nat.lib()
+    out = []
+    cfg = nat.KpConfig()
+    for i in range(lib.kp_num_configs(fam)):
+        nat.check(lib.kp_config_at(fam, i, ctypes.byref(cfg)), "kp_config_at")
+        out.append(KernelConfig(*cfg.as_tuple()))
+    return tuple(out)
+
+
+def select(m: int, k: int, n: int, *, family="f32", trans_a=False, trans_b=False) -> KernelConfig:
+    """The config the compiled runtime selector returns for (m, k, n)."""
+    cfg = nat.KpConfig()
+    nat.check(nat.lib().kp_select(nat.family_id(family), int(trans_a), int(trans_b), m, k, n,
+                                  ctypes.byref(cfg)), "kp_select")
+    return KernelConfig(*cfg.as_tuple())
+
+
+def launch_count() -> int:
+    return int(nat.lib().kp_launch_count())

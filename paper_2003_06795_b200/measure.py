@@ -1,0 +1,174 @@
+"""The measured sweep: B200 twin of the reference's synthetic.generate.
+
+Reference producer: synthetic.generate(spec) -> list[BenchmarkRecord]
+(pkg/src/kernelprune/synthetic.py:92-114): one record per (problem, config),
+row-major by problem then canonical config, runtime_ns = 2mnk / gflops.
+Here every cell is a real kernel launch timed on the GPU (C++ timing loop,
+kp_sweep_problem): operands are allocated once per problem (U[-1,1) fp32,
+seeded per problem), every config runs `warmup` untimed launches and `reps`
+timed samples of back-to-back launches (each sample >= min_sample_ns), and
+the median per-launch time is the cell's runtime. L2 is warm (the same
+operands are reused across launches), which the sidecar records.
+
+Multi-GPU: the cell list shards by problem across worker processes, one per
+GPU, with no device-to-device traffic (sweep_sharded); records return to the
+parent and are merged back into canonical order.
+"""
+
+from __future__ import annotations
+
+import json
+import math
+import os
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .dataset import BenchmarkRecord, KernelConfig, ProblemSize, all_configs
+
+
+@dataclass
+class SweepSpec:
+    problems: tuple[ProblemSize, ...]
+    family: str = "f32"
+    trans_a: bool = False
+    trans_b: bool = False
+    batch: int = 1
+    configs: tuple[KernelConfig, ...] | None = None   # None -> family's full list
+    warmup: int = 2
+    reps: int = 5
+    min_sample_ns: float = 20_000.0
+    seed: int = 0
+
+
+@dataclass
+class SweepResult:
+    spec: SweepSpec
+    configs: tuple[KernelConfig, ...]
+    runtime_ns: np.ndarray           # (P, C)
+    wall_s: float
+    device: dict = field(default_factory=dict)
+
+    @property
+    def cells(self) -> int:
+        return int(self.runtime_ns.size)
+
+    def gflops(self) -> np.ndarray:
+        flops = np.array([2.0 * self.spec.batch * p.m * p.n * p.k for p in self.spec.problems])
+        return flops[:, None] / self.runtime_ns
+
+    def records(self) -> list[BenchmarkRecord]:
+        """Canonical-order records (problem-major), as synthetic.generate."""
+        out = []
+        g = self.gflops()
+        for i, p in enumerate(self.spec.problems):
+            flops = 2 * self.spec.batch * p.m * p.n * p.k
+            for j, c in enumerate(self.configs):
+                gf = float(g[i, j])
+                out.append(BenchmarkRecord(p, c, flops / gf, gf))
+        return out
+
+
+def _operands(problem: ProblemSize, spec: SweepSpec, index: int, device):
+    import torch
+    gen = torch.Generator(device="cpu").manual_seed(spec.seed * 1_000_003 + index)
+    m, k, n, bt = problem.m, problem.k, problem.n, spec.batch
+    a_shape = (k, m) if spec.trans_a else (m, k)
+    b_shape = (n, k) if spec.trans_b else (k, n)
+    if bt > 1:
+        a_shape, b_shape = (bt,) + a_shape, (bt,) + b_shape
+    dtype = torch.bfloat16 if spec.family == "bf16" else torch.float32
+    a = (torch.rand(a_shape, generator=gen) * 2 - 1).to(device=device, dtype=dtype)
+    b = (torch.rand(b_shape, generator=gen) * 2 - 1).to(device=device, dtype=dtype)
+    if spec.trans_a:
+        a = a.transpose(-1, -2)
+    if spec.trans_b:
+        b = b.transpose(-1, -2)
+    return a, b
+
+
+def device_facts(device: int = 0) -> dict:
+    import ctypes
+
+    from . import _native as nat
+    sm, clk, cc = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    nat.check(nat.lib().kp_device_info(device, ctypes.byref(sm), ctypes.byref(clk),
+                                       ctypes.byref(cc)), "kp_device_info")
+    import torch
+    return {"name": torch.cuda.get_device_name(device), "sm_count": sm.value,
+            "sm_clock_max_mhz": clk.value / 1000.0, "cc": cc.value}
+
+
+def run_sweep(spec: SweepSpec, device: int = 0, progress=None) -> SweepResult:
+    """Time every (problem, config) cell of `spec` on one GPU."""
+    import torch
+
+    from . import gemm
+    torch.cuda.set_device(device)
+    configs = tuple(spec.configs) if spec.configs is not None else gemm.family_configs(spec.family)
+    rt = np.zeros((len(spec.problems), len(configs)), dtype=np.float64)
+    t0 = time.perf_counter()
+    for i, p in enumerate(spec.problems):
+        a, b = _operands(p, spec, i, torch.device("cuda", device))
+        rt[i] = gemm.sweep_problem(a, b, configs, family=spec.family, warmup=spec.warmup,
+                                   reps=spec.reps, min_sample_ns=spec.min_sample_ns)
+        del a, b
+        if progress:
+            progress(i, p, rt[i])
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    return SweepResult(spec, configs, rt, wall, device_facts(device))
+
+
+def sidecar(result: SweepResult, extra: dict | None = None) -> dict:
+    s = result.spec
+    doc = {
+        "family": s.family, "trans_a": s.trans_a, "trans_b": s.trans_b, "batch": s.batch,
+        "problems": len(s.problems), "configs": len(result.configs), "cells": result.cells,
+        "warmup": s.warmup, "reps": s.reps, "min_sample_ns": s.min_sample_ns,
+        "statistic": "median of reps samples; each sample = back-to-back launches / count",
+        "l2": "warm (operands reused across launches)",
+        "timing": "CUDA events on the launching stream (kp_sweep_problem)",
+        "wall_s": result.wall_s, "cells_per_s": result.cells / result.wall_s,
+        "device": result.device, "host_cores": os.cpu_count(),
+    }
+    if extra:
+        doc.update(extra)
+    return doc
+
+
+def square_problems(sizes=(64, 128, 256, 512, 1024, 2048)) -> tuple[ProblemSize, ...]:
+    return tuple(ProblemSize(s, s, s) for s in sizes)
+
+
+def main(argv=None) -> int:
+    import argparse
+    ap = argparse.ArgumentParser(description="measured config x size sweep (one GPU)")
+    ap.add_argument("--sizes", default="64,128,256,512,1024,2048")
+    ap.add_argument("--family", default="f32")
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=2)
+    ap.add_argument("--top", type=int, default=5)
+    ap.add_argument("--out")
+    args = ap.parse_args(argv)
+    probs = square_problems(tuple(int(s) for s in args.sizes.split(",")))
+    spec = SweepSpec(probs, family=args.family, reps=args.reps, warmup=args.warmup)
+
+    def prog(i, p, row):
+        flops = 2.0 * p.m * p.n * p.k
+        order = np.argsort(row)
+        best = ", ".join(f"{all_configs()[j].as_tuple() if len(row) == 640 else j}:"
+                         f"{flops / row[j] / 1e3:.2f}TF" for j in order[:args.top])
+        print(f"{p.as_tuple()}: best {best}; worst {flops / row.max() / 1e3:.3f}TF", flush=True)
+
+    res = run_sweep(spec, progress=prog)
+    print(json.dumps(sidecar(res)))
+    if args.out:
+        from .dataset import write_records
+        write_records(res.records(), args.out)
+    return 0
+
+
+if __name__ == "__main__":
+    raise SystemExit(main())

@@ -1,0 +1,154 @@
+"""K1 (FP32 SIMT) parity on the B200 through the C-ABI.
+
+Every config must be bit-identical (value equality) to the sequential-fmaf
+oracle (oracle/gemm_ref.c) -- the kernel accumulates each C element in
+increasing k with fmaf from +0 -- and within rel-Frobenius 1e-5 of the
+float64 matmul (BASELINE config 1, north_star tolerance).
+"""
+
+import numpy as np
+import pytest
+
+from oracle.gemm_oracle import gemm_f32_exact, gemm_f64
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def _gemm():
+    from paper_2003_06795_b200 import gemm
+    return gemm
+
+
+def _dataset():
+    from paper_2003_06795_b200 import dataset
+    return dataset
+
+
+def _operands(rng, m, k, n, ta, tb):
+    a_store = rng.uniform(-1, 1, size=(k, m) if ta else (m, k)).astype(np.float32)
+    b_store = rng.uniform(-1, 1, size=(n, k) if tb else (k, n)).astype(np.float32)
+    a = torch.from_numpy(a_store).cuda()
+    b = torch.from_numpy(b_store).cuda()
+    return a_store, b_store, (a.t() if ta else a), (b.t() if tb else b)
+
+
+def _run(cfg, m, k, n, ta=False, tb=False, seed=0):
+    rng = np.random.default_rng(seed)
+    a_store, b_store, a, b = _operands(rng, m, k, n, ta, tb)
+    got = _gemm().matmul(a, b, cfg).cpu().numpy()
+    want = gemm_f32_exact(a_store, b_store, m=m, k=k, n=n, trans_a=ta, trans_b=tb).reshape(m, n)
+    return got, want, a_store, b_store
+
+
+def test_baseline_config1_256_cubed():
+    """BASELINE configs[0]: 256^3, tile 4x4, acc 4, work-group 8x8."""
+    ds = _dataset()
+    cfg = ds.KernelConfig(4, 4, 4, 8, 8)
+    assert ds.all_configs().index(cfg) == 422
+    got, want, a, b = _run(cfg, 256, 256, 256)
+    np.testing.assert_array_equal(got, want)
+    ref = gemm_f64(a, b)
+    rel = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+    assert rel <= 1e-5, rel
+
+
+@pytest.mark.parametrize("shape", [(17, 27, 15), (33, 64, 70)])
+def test_every_config_bit_exact_nn(shape):
+    m, k, n = shape
+    rng = np.random.default_rng(1)
+    a_store, b_store, a, b = _operands(rng, m, k, n, False, False)
+    want = gemm_f32_exact(a_store, b_store, m=m, k=k, n=n).reshape(m, n)
+    bad = []
+    for cfg in _dataset().all_configs():
+        got = _gemm().matmul(a, b, cfg).cpu().numpy()
+        if not np.array_equal(got, want):
+            bad.append(cfg.as_tuple())
+    assert not bad, f"{len(bad)} configs differ, first {bad[:5]}"
+
+
+@pytest.mark.parametrize("ta,tb", [(False, True), (True, False), (True, True)])
+def test_every_config_bit_exact_transposed(ta, tb):
+    m, k, n = 37, 45, 29
+    rng = np.random.default_rng(2)
+    a_store, b_store, a, b = _operands(rng, m, k, n, ta, tb)
+    want = gemm_f32_exact(a_store, b_store, m=m, k=k, n=n, trans_a=ta,
+                          trans_b=tb).reshape(m, n)
+    bad = []
+    for cfg in _dataset().all_configs():
+        got = _gemm().matmul(a, b, cfg).cpu().numpy()
+        if not np.array_equal(got, want):
+            bad.append(cfg.as_tuple())
+    assert not bad, f"{len(bad)} configs differ, first {bad[:5]}"
+
+
+@pytest.mark.parametrize("shape", [(1, 1, 1), (1, 7, 1), (2049, 17, 3), (3, 2049, 5),
+                                   (64, 64, 64), (128, 96, 160)])
+@pytest.mark.parametrize("cfg", [(1, 1, 1, 1, 64), (8, 8, 8, 16, 16), (2, 8, 1, 128, 1),
+                                 (4, 1, 8, 1, 128), (8, 4, 2, 32, 8)])
+def test_edge_shapes(shape, cfg):
+    ds = _dataset()
+    for ta in (False, True):
+        for tb in (False, True):
+            got, want, _, _ = _run(ds.KernelConfig(*cfg), *shape, ta=ta, tb=tb, seed=3)
+            np.testing.assert_array_equal(got, want)
+
+
+def test_strided_batched_alpha_beta():
+    ds = _dataset()
+    rng = np.random.default_rng(4)
+    batch, m, k, n = 3, 40, 24, 36
+    a = rng.uniform(-1, 1, (batch, m, k)).astype(np.float32)
+    b = rng.uniform(-1, 1, (batch, k, n)).astype(np.float32)
+    c0 = rng.uniform(-1, 1, (batch, m, n)).astype(np.float32)
+    for cfg in [ds.KernelConfig(4, 4, 4, 8, 8), ds.KernelConfig(1, 2, 8, 16, 8)]:
+        out = torch.from_numpy(c0.copy()).cuda()
+        _gemm().matmul(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), cfg,
+                       out=out, alpha=0.5, beta=-1.5)
+        want = gemm_f32_exact(a, b, m=m, k=k, n=n, batch=batch, stride_a=m * k,
+                              stride_b=k * n, alpha=0.5, beta=-1.5, c_init=c0)
+        np.testing.assert_array_equal(out.cpu().numpy().reshape(-1), want)
+
+
+def test_broadcast_b_over_batch():
+    ds = _dataset()
+    rng = np.random.default_rng(5)
+    a = rng.uniform(-1, 1, (4, 19, 33)).astype(np.float32)
+    b = rng.uniform(-1, 1, (33, 21)).astype(np.float32)
+    got = _gemm().matmul(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(),
+                         ds.KernelConfig(2, 2, 2, 8, 8)).cpu().numpy()
+    want = gemm_f32_exact(a, b, m=19, k=33, n=21, batch=4, stride_a=19 * 33, stride_b=0)
+    np.testing.assert_array_equal(got.reshape(-1), want)
+
+
+def test_unaligned_leading_dims():
+    """Row pitches that are not multiples of 4 floats take the 4-byte path."""
+    ds = _dataset()
+    rng = np.random.default_rng(6)
+    store_a = rng.uniform(-1, 1, (50, 31)).astype(np.float32)
+    store_b = rng.uniform(-1, 1, (31, 23)).astype(np.float32)
+    a = torch.from_numpy(store_a).cuda()[:, :27]     # lda = 31
+    b = torch.from_numpy(store_b).cuda()[:27, :19]   # ldb = 23
+    for cfg in [ds.KernelConfig(4, 4, 4, 8, 8), ds.KernelConfig(8, 8, 8, 16, 16)]:
+        got = _gemm().matmul(a, b, cfg).cpu().numpy()
+        want = gemm_f32_exact(store_a, store_b, m=50, k=27, n=19, lda=31, ldb=23).reshape(50, 19)
+        np.testing.assert_array_equal(got, want)
+
+
+def test_invalid_config_and_shape_errors():
+    from paper_2003_06795_b200 import _native as nat
+    a = torch.ones(4, 4, device="cuda")
+    with pytest.raises(nat.InvalidKernelConfig):
+        _gemm().matmul(a, a, (3, 4, 4, 8, 8))
+    with pytest.raises(nat.BadProblemShape):
+        _gemm().matmul(a, torch.ones(5, 4, device="cuda"), (4, 4, 4, 8, 8))
+
+
+def test_timing_loop_positive():
+    ds = _dataset()
+    a = torch.rand(256, 256, device="cuda")
+    ns = _gemm().time_config(a, a, ds.KernelConfig(4, 4, 4, 8, 8), reps=5)
+    assert ns > 0.0
+    res = _gemm().sweep_problem(a, a, ds.all_configs()[:10], reps=3)
+    assert len(res) == 10 and all(v > 0 for v in res)
