@@ -96,21 +96,25 @@ kp_status kp_config_valid(kp_family family, kp_config cfg);
 kp_status kp_gemm(kp_family family, kp_config cfg, const kp_gemm_desc* desc,
                   const void* A, const void* B, float* C, void* stream);
 
-/* Warm up, then time `reps` samples of back-to-back launches (each sample
- * >= min_sample_ns of device time, launch count per sample chosen from the
- * warm-up); *runtime_ns = median per-launch device time (CUDA events on
- * `stream`).  Synchronises `stream`. */
+/* Timing loop (K4).  One untimed launch, one timed launch that sizes the
+ * samples, `warmup`-1 more untimed launches, then `reps` samples of
+ * back-to-back launches (each sample >= min_sample_ns of device time);
+ * *runtime_ns = median per-launch device time (CUDA events on `stream`).
+ * Cell budget: when reps * (one launch) exceeds max_cell_ns (> 0), the extra
+ * warm-ups are skipped and reps shrinks to fit (at least 1 sample), so
+ * hopeless configs on big problems cost ~3 launches.  Synchronises `stream`. */
 kp_status kp_gemm_time(kp_family family, kp_config cfg, const kp_gemm_desc* desc,
                        const void* A, const void* B, float* C,
                        int32_t warmup, int32_t reps, double min_sample_ns,
-                       double* runtime_ns, void* stream);
+                       double max_cell_ns, double* runtime_ns, void* stream);
 
 /* Time every config in `cfgs` on one problem (buffers allocated once by the
  * caller); runtime_ns[i] per config, same timing method as kp_gemm_time. */
 kp_status kp_sweep_problem(kp_family family, const kp_config* cfgs, int32_t n_cfgs,
                            const kp_gemm_desc* desc, const void* A, const void* B,
                            float* C, int32_t warmup, int32_t reps,
-                           double min_sample_ns, double* runtime_ns, void* stream);
+                           double min_sample_ns, double max_cell_ns,
+                           double* runtime_ns, void* stream);
 
 /* ---- runtime selection (generated decision-tree header) --------------- */
 /* Config the compiled selector picks for (m,k,n); KP_ERR_UNSUPPORTED when no

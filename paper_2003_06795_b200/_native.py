@@ -80,10 +80,11 @@ def _declare(lib):
                               c.c_void_p, c.c_void_p]),
         "kp_gemm_time": (c.c_int, [c.c_int, KpConfig, P(KpGemmDesc), c.c_void_p, c.c_void_p,
                                    c.c_void_p, c.c_int32, c.c_int32, c.c_double,
-                                   P(c.c_double), c.c_void_p]),
+                                   c.c_double, P(c.c_double), c.c_void_p]),
         "kp_sweep_problem": (c.c_int, [c.c_int, P(KpConfig), c.c_int32, P(KpGemmDesc),
                                        c.c_void_p, c.c_void_p, c.c_void_p, c.c_int32,
-                                       c.c_int32, c.c_double, P(c.c_double), c.c_void_p]),
+                                       c.c_int32, c.c_double, c.c_double, P(c.c_double),
+                                       c.c_void_p]),
         "kp_select": (c.c_int, [c.c_int, c.c_int32, c.c_int32, c.c_int64, c.c_int64,
                                 c.c_int64, P(KpConfig)]),
         "kp_gemm_auto": (c.c_int, [c.c_int, P(KpGemmDesc), c.c_void_p, c.c_void_p,

@@ -139,14 +139,14 @@ struct EventPool {
 static thread_local EventPool g_events;
 
 static kp_status time_one(kp_family fam, const kp_config& c, const GemmProblem& g, int warmup,
-                          int reps, double min_sample_ns, double* out, cudaStream_t s) {
+                          int reps, double min_sample_ns, double max_cell_ns, double* out,
+                          cudaStream_t s) {
     if (reps < 1) return fail(KP_ERR_INVALID_ARG, "reps must be >= 1");
     kp_status st;
     if ((st = g_events.ensure(2 * size_t(reps) + 2)) != KP_OK) return st;
     cudaEvent_t* ev = g_events.ev.data();
-    for (int w = 0; w < std::max(warmup, 1); ++w)
-        if ((st = run(fam, c, g, s)) != KP_OK) return st;
-    // one timed launch to size the samples
+    // first (cold) launch, then one timed launch to size the samples
+    if ((st = run(fam, c, g, s)) != KP_OK) return st;
     cudaEventRecord(ev[0], s);
     if ((st = run(fam, c, g, s)) != KP_OK) return st;
     cudaEventRecord(ev[1], s);
@@ -154,26 +154,35 @@ static kp_status time_one(kp_family fam, const kp_config& c, const GemmProblem& 
     float one_ms = 0.f;
     cudaEventElapsedTime(&one_ms, ev[0], ev[1]);
     const double one_ns = std::max(1.0, double(one_ms) * 1e6);
+    int nreps = reps;
+    bool budget_hit = false;
+    if (max_cell_ns > 0.0 && one_ns * reps > max_cell_ns) {
+        nreps = std::max(1, int(max_cell_ns / one_ns));
+        budget_hit = true;
+    }
+    if (!budget_hit)
+        for (int w = 1; w < warmup; ++w)
+            if ((st = run(fam, c, g, s)) != KP_OK) return st;
     const int inner = int(std::min(4096.0, std::max(1.0, std::ceil(min_sample_ns / one_ns))));
-    for (int r = 0; r < reps; ++r) {
+    for (int r = 0; r < nreps; ++r) {
         cudaEventRecord(ev[2 + 2 * r], s);
         for (int i = 0; i < inner; ++i)
             if ((st = run(fam, c, g, s)) != KP_OK) return st;
         cudaEventRecord(ev[3 + 2 * r], s);
     }
-    if (cudaEventSynchronize(ev[1 + 2 * reps]) != cudaSuccess) {
+    if (cudaEventSynchronize(ev[1 + 2 * nreps]) != cudaSuccess) {
         const cudaError_t e = cudaGetLastError();
         return fail(KP_ERR_CUDA, std::string("timing sync: ") + cudaGetErrorString(e));
     }
     std::vector<double> per;
-    per.reserve(reps);
-    for (int r = 0; r < reps; ++r) {
+    per.reserve(nreps);
+    for (int r = 0; r < nreps; ++r) {
         float ms = 0.f;
         cudaEventElapsedTime(&ms, ev[2 + 2 * r], ev[3 + 2 * r]);
         per.push_back(double(ms) * 1e6 / inner);
     }
     std::sort(per.begin(), per.end());
-    *out = (reps % 2) ? per[reps / 2] : 0.5 * (per[reps / 2 - 1] + per[reps / 2]);
+    *out = (nreps % 2) ? per[nreps / 2] : 0.5 * (per[nreps / 2 - 1] + per[nreps / 2]);
     return KP_OK;
 }
 
@@ -216,20 +225,20 @@ kp_status kp_gemm(kp_family family, kp_config cfg, const kp_gemm_desc* desc, con
 
 kp_status kp_gemm_time(kp_family family, kp_config cfg, const kp_gemm_desc* desc, const void* A,
                        const void* B, float* C, int32_t warmup, int32_t reps, double min_sample_ns,
-                       double* runtime_ns, void* stream) {
+                       double max_cell_ns, double* runtime_ns, void* stream) {
     kp_status st;
     if (!runtime_ns) return fail(KP_ERR_INVALID_ARG, "null runtime output");
     if ((st = valid_config(family, cfg)) != KP_OK) return st;
     GemmProblem g;
     if ((st = to_problem(desc, A, B, C, &g)) != KP_OK) return st;
-    return time_one(family, cfg, g, warmup, reps, min_sample_ns, runtime_ns,
+    return time_one(family, cfg, g, warmup, reps, min_sample_ns, max_cell_ns, runtime_ns,
                     static_cast<cudaStream_t>(stream));
 }
 
 kp_status kp_sweep_problem(kp_family family, const kp_config* cfgs, int32_t n_cfgs,
                            const kp_gemm_desc* desc, const void* A, const void* B, float* C,
-                           int32_t warmup, int32_t reps, double min_sample_ns, double* runtime_ns,
-                           void* stream) {
+                           int32_t warmup, int32_t reps, double min_sample_ns, double max_cell_ns,
+                           double* runtime_ns, void* stream) {
     if (!cfgs || !runtime_ns || n_cfgs < 0) return fail(KP_ERR_INVALID_ARG, "bad sweep arguments");
     kp_status st;
     GemmProblem g;
@@ -237,8 +246,8 @@ kp_status kp_sweep_problem(kp_family family, const kp_config* cfgs, int32_t n_cf
     for (int32_t i = 0; i < n_cfgs; ++i)
         if ((st = valid_config(family, cfgs[i])) != KP_OK) return st;
     for (int32_t i = 0; i < n_cfgs; ++i) {
-        st = time_one(family, cfgs[i], g, warmup, reps, min_sample_ns, runtime_ns + i,
-                      static_cast<cudaStream_t>(stream));
+        st = time_one(family, cfgs[i], g, warmup, reps, min_sample_ns, max_cell_ns,
+                      runtime_ns + i, static_cast<cudaStream_t>(stream));
         if (st != KP_OK) {
             char buf[96];
             snprintf(buf, sizeof buf, " [config #%d (%u,%u,%u,%u,%u)]", i, cfgs[i].acc,

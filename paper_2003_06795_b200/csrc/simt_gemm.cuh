@@ -19,8 +19,10 @@
 //     thread's rows/cols are laid out so its fragment reads are vectorised
 //     along the operand's contiguous axis and bank-conflict free:
 //       A k-contiguous (NN):  rows ty + i*wg_rows, float-vectors of `acc`
-//       A m-contiguous (TA):  rows ty*row_tile + i, float-vectors of row_tile
-//       B n-contiguous (NN):  cols tx*col_tile + j, float-vectors of col_tile
+//       A m-contiguous (TA):  rows in 4-chunks q*4*wg_rows + ty*4 + e
+//                             (ty*row_tile + i when row_tile < 4)
+//       B n-contiguous (NN):  cols in 4-chunks q*4*wg_cols + tx*4 + e
+//                             (tx*col_tile + j when col_tile < 4)
 //       B k-contiguous (TB):  cols tx + j*wg_cols,  float-vectors of `acc`
 //   * every C element accumulates its K products in increasing k with fmaf,
 //     starting from +0, so results are bit-identical to the sequential-fmaf
@@ -99,6 +101,22 @@ __device__ __forceinline__ void lds(const float* p, float* out) {
             out[4 * q + 2] = v.z; out[4 * q + 3] = v.w;
         }
     }
+}
+
+// Thread -> output row / column maps (see the header comment): operands read
+// along their contiguous axis use 4-wide chunks strided by 4*work-group so a
+// quarter-warp's 16-byte shared loads are contiguous (conflict free).
+template <bool TA, int RT>
+__device__ __forceinline__ int row_of(int i, int ty, int wgr) {
+    if constexpr (!TA) return ty + i * wgr;
+    else if constexpr (RT >= 4) return (i / 4) * 4 * wgr + ty * 4 + (i % 4);
+    else return ty * RT + i;
+}
+template <bool TB, int CT>
+__device__ __forceinline__ int col_of(int j, int tx, int wgc) {
+    if constexpr (TB) return tx + j * wgc;
+    else if constexpr (CT >= 4) return (j / 4) * 4 * wgc + tx * 4 + (j % 4);
+    else return tx * CT + j;
 }
 
 __device__ __forceinline__ float epilogue(float acc, float alpha, float beta, const float* c_old) {
@@ -190,15 +208,28 @@ __global__ void __launch_bounds__(256) simt_gemm_kernel(const Params p) {
 #pragma unroll
                 for (int kk = 0; kk < ACC; ++kk) {
                     float t[RT];
-                    lds<RT>(a_s + (kb + kk) * p.a_stride + ty * RT, t);
+                    if constexpr (RT >= 4) {
+#pragma unroll
+                        for (int q = 0; q < RT / 4; ++q)
+                            lds<4>(a_s + (kb + kk) * p.a_stride + q * 4 * p.wgr + ty * 4, t + 4 * q);
+                    } else {
+                        lds<RT>(a_s + (kb + kk) * p.a_stride + ty * RT, t);
+                    }
 #pragma unroll
                     for (int i = 0; i < RT; ++i) a[i][kk] = t[i];
                 }
             }
             if constexpr (!TB) {
 #pragma unroll
-                for (int kk = 0; kk < ACC; ++kk)
-                    lds<CT>(b_s + (kb + kk) * p.b_stride + tx * CT, b[kk]);
+                for (int kk = 0; kk < ACC; ++kk) {
+                    if constexpr (CT >= 4) {
+#pragma unroll
+                        for (int q = 0; q < CT / 4; ++q)
+                            lds<4>(b_s + (kb + kk) * p.b_stride + q * 4 * p.wgc + tx * 4, b[kk] + 4 * q);
+                    } else {
+                        lds<CT>(b_s + (kb + kk) * p.b_stride + tx * CT, b[kk]);
+                    }
+                }
             } else {
 #pragma unroll
                 for (int j = 0; j < CT; ++j) {
@@ -221,13 +252,13 @@ __global__ void __launch_bounds__(256) simt_gemm_kernel(const Params p) {
     // epilogue: C = alpha*acc (+ beta*C)
 #pragma unroll
     for (int i = 0; i < RT; ++i) {
-        const int m = m0 + (TA ? ty * RT + i : ty + i * p.wgr);
+        const int m = m0 + row_of<TA, RT>(i, ty, p.wgr);
         if (m >= p.M) continue;
         float* crow = C + (int64_t)m * p.ldc;
         if constexpr (!TB && CT >= 4) {
 #pragma unroll
             for (int q = 0; q < CT / 4; ++q) {
-                const int n = n0 + tx * CT + 4 * q;
+                const int n = n0 + q * 4 * p.wgc + tx * 4;
                 if (p.vecC && n + 3 < p.N) {
                     float4 v;
                     if (p.beta == 0.0f) {
@@ -251,7 +282,7 @@ __global__ void __launch_bounds__(256) simt_gemm_kernel(const Params p) {
         } else {
 #pragma unroll
             for (int j = 0; j < CT; ++j) {
-                const int n = n0 + (TB ? tx + j * p.wgc : tx * CT + j);
+                const int n = n0 + col_of<TB, CT>(j, tx, p.wgc);
                 if (n < p.N) crow[n] = epilogue(acc[i][j], p.alpha, p.beta, crow + n);
             }
         }

@@ -143,20 +143,21 @@ def matmul_host(a: np.ndarray, b: np.ndarray, config=None, *, family="f32", devi
 
 
 def time_config(a, b, config, *, family="f32", out=None, warmup: int = 3, reps: int = 10,
-                min_sample_ns: float = 50_000.0) -> float:
+                min_sample_ns: float = 50_000.0, max_cell_ns: float = 0.0) -> float:
     """Median per-launch device time (ns) of one config on one problem."""
     fam = nat.family_id(family)
     desc, a, b, out = describe(a, b, out, 1.0, 0.0, family)
     res = ctypes.c_double()
     nat.check(nat.lib().kp_gemm_time(fam, nat.to_kp_config(config), ctypes.byref(desc),
                                      a.data_ptr(), b.data_ptr(), out.data_ptr(), warmup, reps,
-                                     min_sample_ns, ctypes.byref(res), _stream_handle()),
+                                     min_sample_ns, max_cell_ns, ctypes.byref(res),
+                                     _stream_handle()),
               "kp_gemm_time")
     return res.value
 
 
 def sweep_problem(a, b, configs, *, family="f32", out=None, warmup: int = 2, reps: int = 5,
-                  min_sample_ns: float = 50_000.0) -> list[float]:
+                  min_sample_ns: float = 50_000.0, max_cell_ns: float = 0.0) -> list[float]:
     """Median runtime (ns) of every config on one problem (C++ timing loop)."""
     fam = nat.family_id(family)
     desc, a, b, out = describe(a, b, out, 1.0, 0.0, family)
@@ -164,7 +165,8 @@ def sweep_problem(a, b, configs, *, family="f32", out=None, warmup: int = 2, rep
     res = (ctypes.c_double * len(configs))()
     nat.check(nat.lib().kp_sweep_problem(fam, cfgs, len(configs), ctypes.byref(desc),
                                          a.data_ptr(), b.data_ptr(), out.data_ptr(), warmup,
-                                         reps, min_sample_ns, res, _stream_handle()),
+                                         reps, min_sample_ns, max_cell_ns, res,
+                                         _stream_handle()),
               "kp_sweep_problem")
     return list(res)
 

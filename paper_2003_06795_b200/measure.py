@@ -39,6 +39,7 @@ class SweepSpec:
     warmup: int = 2
     reps: int = 5
     min_sample_ns: float = 20_000.0
+    max_cell_ns: float = 5_000_000.0    # per-cell time budget (kp_gemm_time)
     seed: int = 0
 
 
@@ -112,7 +113,8 @@ def run_sweep(spec: SweepSpec, device: int = 0, progress=None) -> SweepResult:
     for i, p in enumerate(spec.problems):
         a, b = _operands(p, spec, i, torch.device("cuda", device))
         rt[i] = gemm.sweep_problem(a, b, configs, family=spec.family, warmup=spec.warmup,
-                                   reps=spec.reps, min_sample_ns=spec.min_sample_ns)
+                                   reps=spec.reps, min_sample_ns=spec.min_sample_ns,
+                                   max_cell_ns=spec.max_cell_ns)
         del a, b
         if progress:
             progress(i, p, rt[i])
@@ -121,12 +123,125 @@ def run_sweep(spec: SweepSpec, device: int = 0, progress=None) -> SweepResult:
     return SweepResult(spec, configs, rt, wall, device_facts(device))
 
 
+def problem_cost(p: ProblemSize, batch: int = 1) -> float:
+    """Relative sweep cost of one problem: its flops over the reference's
+    analytic throughput averaged over the config space (synthetic.py:73-89),
+    plus a per-config launch floor. Used only to order / balance shards."""
+    from .synthetic import analytic_matrix
+    mean_gflops = float(analytic_matrix([p], all_configs(), 8192.0).mean())
+    return 2.0 * batch * p.m * p.n * p.k / mean_gflops + 640 * 5e3
+
+
+def plan_shards(problems, n_shards: int, batch: int = 1) -> list[list[int]]:
+    """Static longest-processing-time-first partition of problem indices
+    (each shard sorted ascending so merged output keeps canonical order)."""
+    if n_shards < 1:
+        raise ValueError("n_shards must be >= 1")
+    order = sorted(range(len(problems)), key=lambda i: (-problem_cost(problems[i], batch), i))
+    load = [0.0] * n_shards
+    shards: list[list[int]] = [[] for _ in range(n_shards)]
+    for i in order:
+        s = min(range(n_shards), key=lambda j: (load[j], j))
+        shards[s].append(i)
+        load[s] += problem_cost(problems[i], batch)
+    return [sorted(s) for s in shards]
+
+
+def merge_shards(n_problems: int, n_configs: int, parts) -> np.ndarray:
+    """Reassemble {problem index: runtimes row} parts into the (P, C) grid;
+    every problem must arrive exactly once (complete-grid contract,
+    dataset.build_matrix)."""
+    grid = np.full((n_problems, n_configs), np.nan)
+    seen = np.zeros(n_problems, dtype=bool)
+    for part in parts:
+        for i, row in part.items():
+            if seen[i]:
+                raise RuntimeError(f"problem {i} measured twice")
+            seen[i] = True
+            grid[i] = row
+    if not seen.all():
+        raise RuntimeError(f"problems never measured: {np.flatnonzero(~seen).tolist()}")
+    if not np.isfinite(grid).all() or (grid <= 0).any():
+        raise RuntimeError("non-positive or non-finite runtime in sweep")
+    return grid
+
+
+def _worker(device: int, spec: SweepSpec, task_q, result_q) -> None:
+    """One process per GPU: pull problem indices until the queue is empty."""
+    os.environ["CUDA_VISIBLE_DEVICES"] = str(device)
+    try:
+        import torch
+
+        from . import gemm
+        torch.cuda.set_device(0)
+        configs = (tuple(spec.configs) if spec.configs is not None
+                   else gemm.family_configs(spec.family))
+        while True:
+            i = task_q.get()
+            if i is None:
+                break
+            a, b = _operands(spec.problems[i], spec, i, torch.device("cuda", 0))
+            row = gemm.sweep_problem(a, b, configs, family=spec.family, warmup=spec.warmup,
+                                     reps=spec.reps, min_sample_ns=spec.min_sample_ns,
+                                     max_cell_ns=spec.max_cell_ns)
+            del a, b
+            result_q.put(("row", device, i, row))
+        result_q.put(("done", device, device_facts(0), None))
+    except Exception as exc:  # surfaced by the parent; never silently imputed
+        result_q.put(("error", device, repr(exc), None))
+
+
+def run_sharded(spec: SweepSpec, devices) -> SweepResult:
+    """Sweep across several GPUs: a dynamic longest-first work queue of
+    problems, one worker process per GPU, no device-to-device traffic.
+    A worker error aborts the sweep (a failed cell is never imputed)."""
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    task_q, result_q = ctx.Queue(), ctx.Queue()
+    order = sorted(range(len(spec.problems)),
+                   key=lambda i: (-problem_cost(spec.problems[i], spec.batch), i))
+    for i in order:
+        task_q.put(i)
+    for _ in devices:
+        task_q.put(None)
+    t0 = time.perf_counter()
+    procs = [ctx.Process(target=_worker, args=(d, spec, task_q, result_q)) for d in devices]
+    for p in procs:
+        p.start()
+    rows, done, facts = {}, 0, {}
+    try:
+        while done < len(devices):
+            kind, dev, a, b = result_q.get()
+            if kind == "row":
+                rows[a] = b
+            elif kind == "done":
+                done += 1
+                facts[dev] = a
+            else:
+                raise RuntimeError(f"sweep worker on device {dev} failed: {a}")
+    finally:
+        for p in procs:
+            p.join(timeout=30)
+            if p.is_alive():
+                p.terminate()
+    wall = time.perf_counter() - t0
+    from . import gemm
+    n_cfg = len(spec.configs) if spec.configs is not None else None
+    if n_cfg is None:
+        n_cfg = len(next(iter(rows.values())))
+    grid = merge_shards(len(spec.problems), n_cfg, [rows])
+    configs = tuple(spec.configs) if spec.configs is not None else gemm.family_configs(spec.family)
+    first = facts[min(facts)] if facts else {}
+    return SweepResult(spec, configs, grid, wall, dict(first, devices=len(devices)))
+
+
 def sidecar(result: SweepResult, extra: dict | None = None) -> dict:
     s = result.spec
     doc = {
         "family": s.family, "trans_a": s.trans_a, "trans_b": s.trans_b, "batch": s.batch,
         "problems": len(s.problems), "configs": len(result.configs), "cells": result.cells,
         "warmup": s.warmup, "reps": s.reps, "min_sample_ns": s.min_sample_ns,
+        "max_cell_ns": s.max_cell_ns,
         "statistic": "median of reps samples; each sample = back-to-back launches / count",
         "l2": "warm (operands reused across launches)",
         "timing": "CUDA events on the launching stream (kp_sweep_problem)",
