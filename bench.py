@@ -1,0 +1,389 @@
+#!/usr/bin/env python
+"""Headline benchmark: runtime-selected kernel TFLOP/s on the square size set,
+with the full config sweep that defines the per-size oracle-best.
+
+Workload (BASELINE.json configs[1], "full configuration sweep over a small
+square-size set (64-2048) on 1 B200"):
+  1. sweep: every config of the FP32 SIMT family (640) on every square size
+     (64..2048) through the C++ timing loop (kp_sweep_problem) -> the per-size
+     oracle-best and the sweep rate (configs*sizes/s);
+  2. step (timed K times after W warm-ups): one pass over the square sizes,
+     each GEMM dispatched by the compiled decision-tree selector
+     (kp_gemm_auto -> csrc/generated/select_f32_nn.h), L2 flushed (256 MiB
+     write) before every kernel, each kernel timed with CUDA events on the
+     launching stream.
+value = whole-job selected-kernel TFLOP/s (sum of flops / device time, max
+over ranks); e2e = the same metric through the public host-buffer API
+(gemm.matmul_pinned: pinned H2D, kernel, D2H inside the timed region).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+Multi-GPU (torchrun): each rank runs its own replica of the step (weak
+scaling) and sweeps an interleaved 1/N of the configs (no data-path
+collective; timings are gathered on the host).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = ("selected-kernel TFLOP/s (geomean % of oracle-best, % of roofline); "
+          "sweep configs·sizes/s")
+SIZES = (64, 128, 256, 512, 1024, 2048)
+FLUSH_BYTES = 256 << 20
+
+
+def parse_args(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
+    ap.add_argument("--family", default="f32", choices=("f32",))
+    ap.add_argument("--sweep-reps", type=int, default=3)
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0,
+                    help="bounded CPU-baseline sample length")
+    args = ap.parse_args(argv)
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    return args
+
+
+def flops_of(s: int) -> float:
+    return 2.0 * s * s * s
+
+
+# ----------------------------------------------------------- CPU baselines
+
+def cpu_gemm_pass(mats) -> float:
+    """One pass of numpy fp32 a@b over the square set; returns seconds."""
+    t0 = time.perf_counter()
+    for a, b in mats:
+        a @ b
+    return time.perf_counter() - t0
+
+
+def cpu_mats(seed=0):
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    return [(rng.uniform(-1, 1, (s, s)).astype(np.float32),
+             rng.uniform(-1, 1, (s, s)).astype(np.float32)) for s in SIZES]
+
+
+def cpu_baseline(seconds: float) -> dict:
+    """numpy fp32 GEMM (OpenBLAS, all host threads) on the same square set:
+    the CPU restatement of the path (the reference ships no GEMM; its oracle
+    restatement is oracle/gemm_ref.c / numpy), timed for a bounded sample."""
+    mats = cpu_mats()
+    cpu_gemm_pass(mats)  # warm-up
+    passes, spent = 0, 0.0
+    while spent < seconds or passes < 3:
+        spent += cpu_gemm_pass(mats)
+        passes += 1
+    total = passes * sum(flops_of(s) for s in SIZES)
+    return {"value": total / spent / 1e12, "unit": "TFLOP/s", "cores": os.cpu_count(),
+            "kind": "port",
+            "sample": f"{passes} passes of numpy float32 a@b over squares {list(SIZES)} "
+                      f"({spent:.1f} s, OpenBLAS all threads)"}
+
+
+def run_reference(args) -> int:
+    """--impl reference: the CPU implementation of the path (numpy fp32 GEMM
+    over the same workload) on the box's host cores; rank 0 only."""
+    if int(os.environ.get("RANK", "0")) != 0:
+        return 0
+    mats = cpu_mats()
+    for _ in range(args.warmup):
+        cpu_gemm_pass(mats)
+    times = [cpu_gemm_pass(mats) for _ in range(args.steps)]
+    total = sum(times)
+    value = args.steps * sum(flops_of(s) for s in SIZES) / total / 1e12
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "square GEMM pass 64..2048 (fp32, NN)", "sizes": list(SIZES)},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": os.cpu_count(),
+                         "kind": "port",
+                         "sample": f"{args.steps} timed passes of numpy float32 a@b "
+                                   f"(OpenBLAS, all host threads)"},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# -------------------------------------------------------------- GPU helpers
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms."""
+
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self):
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self, gpu_index: int) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        mhz, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in Path(self.path).read_text().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9 or f[0] != str(gpu_index):
+                continue
+            try:
+                mhz.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for name, val in zip(names, f[5:9]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(mhz) if mhz else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(mhz)}
+
+
+def gpu_index() -> int:
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if vis:
+        ids = [v for v in vis.split(",") if v.strip()]
+        if local < len(ids) and ids[local].strip().isdigit():
+            return int(ids[local])
+    return local
+
+
+def traffic_for(cfg, size):
+    """dram bytes/launch of this kernel from the committed ncu summary, if any."""
+    path = ROOT / "profiles" / "ncu_traffic.json"
+    if not path.exists():
+        return None
+    try:
+        doc = json.loads(path.read_text())
+    except ValueError:
+        return None
+    key = f"f32_nn_{size}_{'-'.join(str(v) for v in cfg.as_tuple())}"
+    ent = doc.get(key)
+    return None if ent is None else ent.get("dram_bytes")
+
+
+def run_gpu(args) -> int:
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2003_06795_b200 import gemm
+    from paper_2003_06795_b200.dataset import all_configs
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    gloo = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        gloo = dist.new_group(backend="gloo")
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    gen = torch.Generator(device="cpu").manual_seed(1234 + rank)
+    probs = []
+    for s in SIZES:
+        a = (torch.rand((s, s), generator=gen) * 2 - 1).to(dev)
+        b = (torch.rand((s, s), generator=gen) * 2 - 1).to(dev)
+        c = torch.empty((s, s), device=dev)
+        probs.append((s, a, b, c))
+    selected = [gemm.select(s, s, s) for s in SIZES]  # raises if no selector compiled in
+
+    # ---- 1. sweep (interleaved config shard per rank) -----------------------
+    configs = all_configs()
+    mine = [j for j in range(len(configs)) if j % world == rank]
+    sweep = {}
+    barrier()
+    t0 = time.perf_counter()
+    if not args.no_sweep:
+        for i, (s, a, b, c) in enumerate(probs):
+            res = gemm.sweep_problem(a, b, [configs[j] for j in mine], out=c, warmup=1,
+                                     reps=args.sweep_reps, min_sample_ns=20_000.0,
+                                     max_cell_ns=5e6)
+            for j, ns in zip(mine, res):
+                sweep[(i, j)] = ns
+    barrier()
+    sweep_wall = time.perf_counter() - t0
+    if world > 1:
+        walls = [None] * world
+        dist.all_gather_object(walls, sweep_wall, group=gloo)
+        parts = [None] * world
+        dist.all_gather_object(parts, sweep, group=gloo)
+        sweep_wall = max(walls)
+        for part in parts:
+            sweep.update(part)
+
+    # ---- peaks for the roofline -------------------------------------------
+    import ctypes
+
+    from paper_2003_06795_b200 import _native as nat
+    peak = ctypes.c_double()
+    nat.check(nat.lib().kp_fp32_peak(ctypes.byref(peak), None), "kp_fp32_peak")
+
+    # ---- 2. timed steps: selected kernels, L2 flushed before each ---------
+    flush = torch.empty(FLUSH_BYTES // 4, device=dev)
+    stream = torch.cuda.current_stream()
+    n_steps = args.warmup + args.steps
+    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in SIZES] for _ in range(n_steps)]
+    clocks = ClockSampler()
+    launches0 = None
+    for step in range(n_steps):
+        if step == args.warmup:
+            barrier()
+            clocks.start()
+            launches0 = gemm.launch_count()
+        for i, (s, a, b, c) in enumerate(probs):
+            flush.zero_()
+            ev[step][i][0].record(stream)
+            gemm.matmul(a, b, None, out=c)
+            ev[step][i][1].record(stream)
+    barrier()
+    launches = gemm.launch_count() - launches0
+    clk = clocks.stop(gpu_index())
+    per_size_ms = np.array([[ev[st][i][0].elapsed_time(ev[st][i][1]) for i in range(len(SIZES))]
+                            for st in range(args.warmup, n_steps)])
+    total_ms = float(per_size_ms.sum())
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        lt = torch.tensor([launches], device=dev, dtype=torch.int64)
+        dist.all_reduce(lt)
+        launches = int(lt.item())
+    step_flops = sum(flops_of(s) for s in SIZES)
+    value = world * args.steps * step_flops / (total_ms * 1e-3) / 1e12
+
+    # ---- 3. e2e through the host-buffer API --------------------------------
+    host = []
+    for s, a, b, c in probs:
+        host.append((a.cpu().pin_memory(), b.cpu().pin_memory(),
+                     torch.empty((s, s), pin_memory=True)))
+    for _ in range(args.warmup):
+        for ha, hb, hc in host:
+            gemm.matmul_pinned(ha, hb, hc)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        for ha, hb, hc in host:
+            gemm.matmul_pinned(ha, hb, hc)
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = world * args.steps * step_flops / e2e_s / 1e12
+    h2d = sum(2 * 4 * s * s for s in SIZES)
+    d2h = sum(4 * s * s for s in SIZES)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    # ---- per-size report, % of oracle-best ---------------------------------
+    mean_ms = per_size_ms.mean(axis=0)
+    per_size, ratios = [], []
+    for i, s in enumerate(SIZES):
+        entry = {"size": s, "config": list(selected[i].as_tuple()),
+                 "tflops": flops_of(s) / (mean_ms[i] * 1e-3) / 1e12}
+        if sweep:
+            row = np.array([sweep[(i, j)] for j in range(len(configs))])
+            jbest = int(row.argmin())
+            jsel = configs.index(selected[i])
+            ratios.append(row[jbest] / row[jsel])
+            entry.update(best_config=list(configs[jbest].as_tuple()),
+                         best_tflops_warm=flops_of(s) / row[jbest] / 1e3,
+                         selected_tflops_warm=flops_of(s) / row[jsel] / 1e3)
+        per_size.append(entry)
+    pct_best = (100.0 * math.exp(sum(math.log(r) for r in ratios) / len(ratios))
+                if ratios else None)
+    dom = int(mean_ms.argmax())  # kernel with the largest share of the step
+    achieved = flops_of(SIZES[dom]) / (mean_ms[dom] * 1e-3) / 1e12
+    roofline = {"bound": "fp32-ffma", "achieved": achieved, "peak": peak.value,
+                "unit": "TFLOP/s", "frac": achieved / peak.value,
+                "traffic": traffic_for(selected[dom], SIZES[dom]),
+                "kernel": f"simt_gemm {list(selected[dom].as_tuple())} @ {SIZES[dom]}^3",
+                "share_of_step": float(mean_ms[dom] / mean_ms.sum()),
+                "peak_source": "measured FFMA microbenchmark (kp_fp32_peak) on this GPU; "
+                               "MEASURED_PEAKS.json has no fp32 SIMT figure"}
+    line = {
+        "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": "640-config sweep + runtime-selected FP32 SIMT GEMM pass over "
+                               "squares 64..2048 (NN)",
+                   "sizes": list(SIZES), "selector": "csrc/generated/select_f32_nn.h",
+                   "l2": f"flushed before every timed kernel ({FLUSH_BYTES >> 20} MiB write)",
+                   "parallelism": f"replicas x{world}"},
+        "pct_oracle_best": pct_best,
+        "sweep": {"cells": len(sweep), "wall_s": sweep_wall,
+                  "cells_per_s": len(sweep) / sweep_wall if sweep else None,
+                  "timing": "warm L2, median of reps, C++ loop (kp_sweep_problem)"},
+        "per_size": per_size,
+        "roofline": roofline,
+        "e2e": {"value": e2e_value, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h,
+                "path": "gemm.matmul_pinned: pinned H2D + kp_gemm_auto + D2H + sync"},
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    if world == 1:
+        line["cpu_baseline"] = cpu_baseline(args.cpu_seconds)
+    print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main(argv=None) -> int:
+    args = parse_args(argv)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -134,6 +134,9 @@ int64_t     kp_launch_count(void);
  * compute capability (major*10+minor). */
 kp_status   kp_device_info(int32_t device, int32_t* sm_count, int32_t* sm_clock_khz,
                            int32_t* cc);
+/* Measured FP32 FFMA throughput of the current device (TFLOP/s, best of 5
+ * full-chip launches at the clocks of the moment): the K1 roofline peak. */
+kp_status   kp_fp32_peak(double* tflops, void* stream);
 
 #ifdef __cplusplus
 }

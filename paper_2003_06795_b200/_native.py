@@ -28,7 +28,8 @@ KP_ERR_INVALID_ARG = 6
 # every symbol include/kp_abi.h declares (checked by tests/test_abi.py)
 EXPORTS = ("kp_abi_version", "kp_num_configs", "kp_config_at", "kp_config_valid",
            "kp_gemm", "kp_gemm_time", "kp_sweep_problem", "kp_select", "kp_gemm_auto",
-           "kp_status_string", "kp_last_error", "kp_launch_count", "kp_device_info")
+           "kp_status_string", "kp_last_error", "kp_launch_count", "kp_device_info",
+           "kp_fp32_peak")
 
 
 class KpConfig(ctypes.Structure):
@@ -93,6 +94,7 @@ def _declare(lib):
         "kp_last_error": (c.c_char_p, []),
         "kp_launch_count": (c.c_int64, []),
         "kp_device_info": (c.c_int, [c.c_int32, P(c.c_int32), P(c.c_int32), P(c.c_int32)]),
+        "kp_fp32_peak": (c.c_int, [P(c.c_double), c.c_void_p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -43,7 +43,8 @@ def nvcc() -> str:
 def _units():
     """(object name, source, extra defines) for every translation unit."""
     units = [("kp_abi.o", CSRC / "kp_abi.cu", []),
-             ("tc_gemm.o", CSRC / "tc_gemm.cu", [])]
+             ("tc_gemm.o", CSRC / "tc_gemm.cu", []),
+             ("peak.o", CSRC / "peak.cu", [])]
     for acc in TILES:
         for rt in TILES:
             units.append((f"simt_a{acc}_r{rt}.o", CSRC / "simt_inst.cu",

@@ -85,6 +85,61 @@ __device__ __forceinline__ void load_tile(float* s, int s_stride, const float* g
     }
 }
 
+// Copy one pipeline stage of an operand tile into shared memory. The tile is
+// rows x cols (cols = 1 << log_cols contiguous in global memory, row pitch
+// ld); KCOL says whether K runs along the columns (A normal, B transposed) or
+// along the rows (A transposed, B normal); `lim` is the in-range extent of the
+// non-K axis. Fast path (16-byte copies, >= one thread per 4-float column
+// chunk, <= 8 chunks per thread): a thread's chunks share one column position
+// and sit dr rows apart, so the per-stage cost is a few integer ops plus the
+// cp.async instructions; everything else is block-uniform. Stateless on
+// purpose: keeping per-thread copy plans live costs registers the 8x8
+// accumulator tiles need (measured: 128 -> 200+ registers).
+template <bool KCOL>
+__device__ __forceinline__ void copy_stage(float* s, int s_stride, const float* tile, int64_t ld,
+                                           int rows, int log_cols, int lim, int k0, int K,
+                                           bool vec, int tid, int nthr) {
+    const int log_cpr = log_cols - 2;
+    if (vec && log_cpr >= 0 && (nthr >> log_cpr) > 0 && (rows << log_cpr) <= 8 * nthr) {
+        const int r0 = tid >> log_cpr;
+        const int c0 = (tid & ((1 << log_cpr) - 1)) << 2;
+        const int dr = nthr >> log_cpr;
+        const int total = rows << log_cpr;
+        const int n = total >= nthr ? total / nthr : (tid < total ? 1 : 0);
+        float* sp = s + r0 * s_stride + c0;
+        const int s_step = dr * s_stride;
+        const int64_t g_step = (int64_t)dr * ld;
+        if constexpr (KCOL) {
+            const float* gp = tile + (int64_t)r0 * ld + c0 + k0;
+            const int kbytes = min(max(K - k0 - c0, 0), 4) * 4;
+            const int rv = lim - r0;  // chunk c in range while c*dr < rv
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                if (c < n) {
+                    const int bytes = c * dr < rv ? kbytes : 0;
+                    cp_async16(sp + c * s_step, bytes ? gp + c * g_step : tile, bytes);
+                }
+            }
+        } else {
+            const float* gp = tile + (int64_t)(r0 + k0) * ld + c0;
+            const int cbytes = min(max(lim - c0, 0), 4) * 4;
+            const int kv = K - k0 - r0;  // chunk c in range while c*dr < kv
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                if (c < n) {
+                    const int bytes = c * dr < kv ? cbytes : 0;
+                    cp_async16(sp + c * s_step, bytes ? gp + c * g_step : tile, bytes);
+                }
+            }
+        }
+    } else if constexpr (KCOL) {
+        load_tile(s, s_stride, tile + k0, ld, rows, log_cols, lim, K - k0, vec, tid, nthr);
+    } else {
+        load_tile(s, s_stride, tile + (int64_t)k0 * ld, ld, rows, log_cols, K - k0, lim, vec, tid,
+                  nthr);
+    }
+}
+
 // Vector shared-memory load of W consecutive floats (W in 1,2,4,8).
 template <int W>
 __device__ __forceinline__ void lds(const float* p, float* out) {
@@ -125,7 +180,7 @@ __device__ __forceinline__ float epilogue(float acc, float alpha, float beta, co
 }
 
 template <int ACC, int RT, int CT, bool TA, bool TB>
-__global__ void __launch_bounds__(256) simt_gemm_kernel(const Params p) {
+__global__ void __launch_bounds__(256, 2) simt_gemm_kernel(const Params p) {
     extern __shared__ __align__(16) float smem[];
     const int tid = threadIdx.x;
     const int nthr = p.wgr * p.wgc;
@@ -155,22 +210,24 @@ __global__ void __launch_bounds__(256) simt_gemm_kernel(const Params p) {
     float* sB = smem + p.stages * p.a_elems;
     const int KT = (p.K + BK - 1) >> LOG_BK;
 
+    // A: k-contiguous rows of m (normal) or m-contiguous rows of k (TA);
+    // B: n-contiguous rows of k (normal) or k-contiguous rows of n (TB).
     auto issue = [&](int kt, int stage) {
         const int k0 = kt << LOG_BK;
         float* a_dst = sA + stage * p.a_elems;
         float* b_dst = sB + stage * p.b_elems;
         if constexpr (!TA)
-            load_tile(a_dst, p.a_stride, A + (int64_t)m0 * p.lda + k0, p.lda, BM, LOG_BK,
-                      p.M - m0, p.K - k0, p.vecA, tid, nthr);
+            copy_stage<true>(a_dst, p.a_stride, A + (int64_t)m0 * p.lda, p.lda, BM, LOG_BK,
+                             p.M - m0, k0, p.K, p.vecA, tid, nthr);
         else
-            load_tile(a_dst, p.a_stride, A + (int64_t)k0 * p.lda + m0, p.lda, BK, p.log_bm,
-                      p.K - k0, p.M - m0, p.vecA, tid, nthr);
+            copy_stage<false>(a_dst, p.a_stride, A + m0, p.lda, BK, p.log_bm, p.M - m0, k0, p.K,
+                              p.vecA, tid, nthr);
         if constexpr (!TB)
-            load_tile(b_dst, p.b_stride, B + (int64_t)k0 * p.ldb + n0, p.ldb, BK, p.log_bn,
-                      p.K - k0, p.N - n0, p.vecB, tid, nthr);
+            copy_stage<false>(b_dst, p.b_stride, B + n0, p.ldb, BK, p.log_bn, p.N - n0, k0, p.K,
+                              p.vecB, tid, nthr);
         else
-            load_tile(b_dst, p.b_stride, B + (int64_t)n0 * p.ldb + k0, p.ldb, BN, LOG_BK,
-                      p.N - n0, p.K - k0, p.vecB, tid, nthr);
+            copy_stage<true>(b_dst, p.b_stride, B + (int64_t)n0 * p.ldb, p.ldb, BN, LOG_BK,
+                             p.N - n0, k0, p.K, p.vecB, tid, nthr);
     };
 
     float acc[RT][CT];
@@ -185,17 +242,16 @@ __global__ void __launch_bounds__(256) simt_gemm_kernel(const Params p) {
         cp_async_commit();
     }
 
+    int rd = 0, wr = S - 1;  // stage being read / written
     for (int kt = 0; kt < KT; ++kt) {
         if (S == 3) cp_async_wait<1>(); else cp_async_wait<0>();
         __syncthreads();
-        {
-            const int nk = kt + S - 1;
-            if (nk < KT) issue(nk, nk % S);
-            cp_async_commit();
-        }
-        const int stage = kt % S;
-        const float* a_s = sA + stage * p.a_elems;
-        const float* b_s = sB + stage * p.b_elems;
+        if (kt + S - 1 < KT) issue(kt + S - 1, wr);
+        cp_async_commit();
+        wr = (wr + 1 == S) ? 0 : wr + 1;
+        const float* a_s = sA + rd * p.a_elems;
+        const float* b_s = sB + rd * p.b_elems;
+        rd = (rd + 1 == S) ? 0 : rd + 1;
 #pragma unroll
         for (int kb = 0; kb < BK; kb += ACC) {
             float a[RT][ACC];

@@ -142,6 +142,22 @@ def matmul_host(a: np.ndarray, b: np.ndarray, config=None, *, family="f32", devi
     return host.numpy()
 
 
+def matmul_pinned(a_host, b_host, out_host, config=None, *, family="f32"):
+    """End-to-end call on pinned host tensors: H2D copies, the kernel (runtime
+    selector when config is None), D2H copy, stream synchronise."""
+    torch = _torch()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    want = _family_dtype(nat.family_id(family))
+    da = a_host.to(dev, non_blocking=True)
+    db = b_host.to(dev, non_blocking=True)
+    if da.dtype != want:
+        da, db = da.to(want), db.to(want)
+    dc = matmul(da, db, config, family=family)
+    out_host.copy_(dc, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return out_host
+
+
 def time_config(a, b, config, *, family="f32", out=None, warmup: int = 3, reps: int = 10,
                 min_sample_ns: float = 50_000.0, max_cell_ns: float = 0.0) -> float:
     """Median per-launch device time (ns) of one config on one problem."""
