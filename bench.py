@@ -203,7 +203,7 @@ def run_gpu(args) -> int:
     import torch
     import torch.distributed as dist
 
-    from paper_2003_06795_b200 import gemm
+    from paper_2003_06795_b200 import gemm, measure
     from paper_2003_06795_b200.dataset import all_configs
 
     rank = int(os.environ.get("RANK", "0"))
@@ -232,7 +232,7 @@ def run_gpu(args) -> int:
 
     # ---- 1. sweep (interleaved config shard per rank) -----------------------
     configs = all_configs()
-    mine = [j for j in range(len(configs)) if j % world == rank]
+    mine = measure.config_shard(len(configs), rank, world)
     sweep = {}
     barrier()
     t0 = time.perf_counter()
@@ -248,11 +248,8 @@ def run_gpu(args) -> int:
     if world > 1:
         walls = [None] * world
         dist.all_gather_object(walls, sweep_wall, group=gloo)
-        parts = [None] * world
-        dist.all_gather_object(parts, sweep, group=gloo)
         sweep_wall = max(walls)
-        for part in parts:
-            sweep.update(part)
+    sweep = measure.gather_cells(sweep, world, gloo)
 
     # ---- peaks for the roofline -------------------------------------------
     import ctypes

@@ -6,24 +6,22 @@
 //   * each thread (work item) owns a row_tile x col_tile block of C,
 //   * a work-group of wg_rows x wg_cols threads owns a
 //     (row_tile*wg_rows) x (col_tile*wg_cols) block of C,
-//   * K is consumed `acc` values per register step.
+//   * K is consumed `acc` values per register step: a thread loads `acc`
+//     k-slices of its A and B fragments, then issues acc*row_tile*col_tile
+//     FFMAs ((row_tile+col_tile)*acc fragment registers).
 // row_tile/col_tile/acc are template parameters (64 kernels per operand
 // layout); the work-group shape is a runtime launch parameter, as in the paper
 // ("can be set at runtime and do not require additional kernels").
 //
 // B200 mapping:
-//   * global -> shared through a 2/3-stage cp.async ring (16-byte copies when
-//     rows are 16-byte aligned, 4-byte zero-filling copies otherwise), shared
-//     K depth BK = 16 (a multiple of every acc);
-//   * shared tiles keep the operand's global layout (no transposes), and each
-//     thread's rows/cols are laid out so its fragment reads are vectorised
-//     along the operand's contiguous axis and bank-conflict free:
-//       A k-contiguous (NN):  rows ty + i*wg_rows, float-vectors of `acc`
-//       A m-contiguous (TA):  rows in 4-chunks q*4*wg_rows + ty*4 + e
-//                             (ty*row_tile + i when row_tile < 4)
-//       B n-contiguous (NN):  cols in 4-chunks q*4*wg_cols + tx*4 + e
-//                             (tx*col_tile + j when col_tile < 4)
-//       B k-contiguous (TB):  cols tx + j*wg_cols,  float-vectors of `acc`
+//   * shared memory holds both operands K-major (As[k][m], Bs[k][n]) with a
+//     K depth of BK = 16 per stage in a 2/3-stage cp.async ring; m/n-contiguous
+//     sources (A transposed, B normal) are copied with 16-byte cp.async,
+//     k-contiguous sources (A normal, B transposed) are transposed on the fly
+//     by 4-byte cp.async (coalesced along k, zero-filling tails);
+//   * a thread's rows (cols) are 4-wide chunks strided by 4*wg_rows
+//     (4*wg_cols), so every fragment read is a conflict-free LDS.128 and every
+//     C store a 16-byte STG;
 //   * every C element accumulates its K products in increasing k with fmaf,
 //     starting from +0, so results are bit-identical to the sequential-fmaf
 //     oracle (oracle/gemm_ref.c); K/M/N tails are zero-filled in shared memory.
@@ -51,96 +49,85 @@ struct Params {
     int stages;
     int vecA, vecB, vecC;
     int tiles_m, tiles_n;
-    int a_stride, b_stride;  // floats per shared row
+    int a_stride, b_stride;  // floats per shared row (BM + pad, BN + pad)
     int a_elems, b_elems;    // floats per stage
 };
 
-// Cooperative copy of a rows x cols block (cols = 1 << log_cols contiguous in
-// global memory) into shared memory with row stride s_stride. Elements with
-// r >= row_lim or c >= col_lim are written as zero.
-__device__ __forceinline__ void load_tile(float* s, int s_stride, const float* g, int64_t g_ld,
-                                          int rows, int log_cols, int row_lim, int col_lim,
-                                          bool vec, int tid, int nthr) {
+// Copy a BK x cols block whose rows are K (source row pitch ld, element
+// (k, c) at src[k*ld + c], cols = 1 << log_cols) into s[k*s_stride + c].
+// Elements with k >= kv or c >= cv are written as zero.
+__device__ __forceinline__ void copy_direct(float* s, int s_stride, const float* src, int64_t ld,
+                                            int log_cols, int cv, int kv, bool vec, int tid,
+                                            int nthr) {
     if (vec && log_cols >= 2) {
         const int log_cpr = log_cols - 2;
-        const int total = rows << log_cpr;
+        const int total = BK << log_cpr;
+        if ((nthr >> log_cpr) > 0 && total <= 8 * nthr) {
+            // fast: every chunk of this thread sits in one column, dr rows apart
+            const int r0 = tid >> log_cpr;
+            const int c0 = (tid & ((1 << log_cpr) - 1)) << 2;
+            const int dr = nthr >> log_cpr;
+            const int n = total >= nthr ? total / nthr : (tid < total ? 1 : 0);
+            const int cbytes = min(max(cv - c0, 0), 4) * 4;
+            const float* gp = src + (int64_t)r0 * ld + c0;
+            float* sp = s + r0 * s_stride + c0;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                if (c < n) {
+                    const int bytes = r0 + c * dr < kv ? cbytes : 0;
+                    cp_async16(sp + c * dr * s_stride, bytes ? gp + (int64_t)c * dr * ld : src, bytes);
+                }
+            }
+            return;
+        }
         for (int idx = tid; idx < total; idx += nthr) {
             const int r = idx >> log_cpr;
             const int c = (idx & ((1 << log_cpr) - 1)) << 2;
-            int valid = 0;
-            if (r < row_lim) valid = min(max(col_lim - c, 0), 4);
-            const float* src = valid ? g + (int64_t)r * g_ld + c : g;
-            cp_async16(s + r * s_stride + c, src, valid * 4);
+            const int bytes = r < kv ? min(max(cv - c, 0), 4) * 4 : 0;
+            cp_async16(s + r * s_stride + c, bytes ? src + (int64_t)r * ld + c : src, bytes);
         }
-    } else {
-        const int cols = 1 << log_cols;
-        const int total = rows << log_cols;
-        for (int idx = tid; idx < total; idx += nthr) {
-            const int r = idx >> log_cols;
-            const int c = idx & (cols - 1);
-            const bool ok = (r < row_lim) && (c < col_lim);
-            const float* src = ok ? g + (int64_t)r * g_ld + c : g;
-            cp_async4(s + r * s_stride + c, src, ok ? 4 : 0);
-        }
+        return;
+    }
+    const int total = BK << log_cols;
+    for (int idx = tid; idx < total; idx += nthr) {
+        const int r = idx >> log_cols;
+        const int c = idx & ((1 << log_cols) - 1);
+        const bool ok = r < kv && c < cv;
+        cp_async4(s + r * s_stride + c, ok ? src + (int64_t)r * ld + c : src, ok ? 4 : 0);
     }
 }
 
-// Copy one pipeline stage of an operand tile into shared memory. The tile is
-// rows x cols (cols = 1 << log_cols contiguous in global memory, row pitch
-// ld); KCOL says whether K runs along the columns (A normal, B transposed) or
-// along the rows (A transposed, B normal); `lim` is the in-range extent of the
-// non-K axis. Fast path (16-byte copies, >= one thread per 4-float column
-// chunk, <= 8 chunks per thread): a thread's chunks share one column position
-// and sit dr rows apart, so the per-stage cost is a few integer ops plus the
-// cp.async instructions; everything else is block-uniform. Stateless on
-// purpose: keeping per-thread copy plans live costs registers the 8x8
-// accumulator tiles need (measured: 128 -> 200+ registers).
-template <bool KCOL>
-__device__ __forceinline__ void copy_stage(float* s, int s_stride, const float* tile, int64_t ld,
-                                           int rows, int log_cols, int lim, int k0, int K,
-                                           bool vec, int tid, int nthr) {
-    const int log_cpr = log_cols - 2;
-    if (vec && log_cpr >= 0 && (nthr >> log_cpr) > 0 && (rows << log_cpr) <= 8 * nthr) {
-        const int r0 = tid >> log_cpr;
-        const int c0 = (tid & ((1 << log_cpr) - 1)) << 2;
-        const int dr = nthr >> log_cpr;
-        const int total = rows << log_cpr;
-        const int n = total >= nthr ? total / nthr : (tid < total ? 1 : 0);
-        float* sp = s + r0 * s_stride + c0;
-        const int s_step = dr * s_stride;
-        const int64_t g_step = (int64_t)dr * ld;
-        if constexpr (KCOL) {
-            const float* gp = tile + (int64_t)r0 * ld + c0 + k0;
-            const int kbytes = min(max(K - k0 - c0, 0), 4) * 4;
-            const int rv = lim - r0;  // chunk c in range while c*dr < rv
+// Transposing copy: source rows are the non-K axis (element (r, k) at
+// src[r*ld + k], rows = 1 << log_rows), destination K-major s[k*s_stride + r].
+// 4-byte cp.async with consecutive threads along k (coalesced reads); nthr is
+// a multiple of BK so each thread keeps one k and strides over rows.
+__device__ __forceinline__ void copy_transpose(float* s, int s_stride, const float* src, int64_t ld,
+                                               int log_rows, int rv, int kv, int tid, int nthr) {
+    const int k = tid & (BK - 1);
+    const int r0 = tid >> LOG_BK;
+    const int rstep = nthr >> LOG_BK;
+    const int rows = 1 << log_rows;
+    const bool kin = k < kv;
+    const float* gp = src + k;
+    float* sp = s + k * s_stride;
+    if (rows <= 16 * rstep) {
 #pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                if (c < n) {
-                    const int bytes = c * dr < rv ? kbytes : 0;
-                    cp_async16(sp + c * s_step, bytes ? gp + c * g_step : tile, bytes);
-                }
-            }
-        } else {
-            const float* gp = tile + (int64_t)(r0 + k0) * ld + c0;
-            const int cbytes = min(max(lim - c0, 0), 4) * 4;
-            const int kv = K - k0 - r0;  // chunk c in range while c*dr < kv
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                if (c < n) {
-                    const int bytes = c * dr < kv ? cbytes : 0;
-                    cp_async16(sp + c * s_step, bytes ? gp + c * g_step : tile, bytes);
-                }
+        for (int c = 0; c < 16; ++c) {
+            const int r = r0 + c * rstep;
+            if (r < rows) {
+                const bool ok = kin && r < rv;
+                cp_async4(sp + r, ok ? gp + (int64_t)r * ld : src, ok ? 4 : 0);
             }
         }
-    } else if constexpr (KCOL) {
-        load_tile(s, s_stride, tile + k0, ld, rows, log_cols, lim, K - k0, vec, tid, nthr);
-    } else {
-        load_tile(s, s_stride, tile + (int64_t)k0 * ld, ld, rows, log_cols, K - k0, lim, vec, tid,
-                  nthr);
+        return;
+    }
+    for (int r = r0; r < rows; r += rstep) {
+        const bool ok = kin && r < rv;
+        cp_async4(sp + r, ok ? gp + (int64_t)r * ld : src, ok ? 4 : 0);
     }
 }
 
-// Vector shared-memory load of W consecutive floats (W in 1,2,4,8).
+// Vector shared-memory load of W consecutive floats (W in 1,2,4).
 template <int W>
 __device__ __forceinline__ void lds(const float* p, float* out) {
     if constexpr (W == 1) {
@@ -149,29 +136,26 @@ __device__ __forceinline__ void lds(const float* p, float* out) {
         const float2 v = *reinterpret_cast<const float2*>(p);
         out[0] = v.x; out[1] = v.y;
     } else {
-#pragma unroll
-        for (int q = 0; q < W / 4; ++q) {
-            const float4 v = reinterpret_cast<const float4*>(p)[q];
-            out[4 * q + 0] = v.x; out[4 * q + 1] = v.y;
-            out[4 * q + 2] = v.z; out[4 * q + 3] = v.w;
-        }
+        const float4 v = *reinterpret_cast<const float4*>(p);
+        out[0] = v.x; out[1] = v.y; out[2] = v.z; out[3] = v.w;
     }
 }
 
-// Thread -> output row / column maps (see the header comment): operands read
-// along their contiguous axis use 4-wide chunks strided by 4*work-group so a
-// quarter-warp's 16-byte shared loads are contiguous (conflict free).
-template <bool TA, int RT>
-__device__ __forceinline__ int row_of(int i, int ty, int wgr) {
-    if constexpr (!TA) return ty + i * wgr;
-    else if constexpr (RT >= 4) return (i / 4) * 4 * wgr + ty * 4 + (i % 4);
-    else return ty * RT + i;
+// The T values thread `t` owns along one axis of a K-major tile row: 4-wide
+// chunks strided by 4*wg when T >= 4, else T contiguous values.
+template <int T>
+__device__ __forceinline__ void load_frag(const float* row, int t, int wg, float* out) {
+    if constexpr (T >= 4) {
+#pragma unroll
+        for (int q = 0; q < T / 4; ++q) lds<4>(row + q * 4 * wg + t * 4, out + 4 * q);
+    } else {
+        lds<T>(row + t * T, out);
+    }
 }
-template <bool TB, int CT>
-__device__ __forceinline__ int col_of(int j, int tx, int wgc) {
-    if constexpr (TB) return tx + j * wgc;
-    else if constexpr (CT >= 4) return (j / 4) * 4 * wgc + tx * 4 + (j % 4);
-    else return tx * CT + j;
+template <int T>
+__device__ __forceinline__ int frag_index(int i, int t, int wg) {
+    if constexpr (T >= 4) return (i / 4) * 4 * wg + t * 4 + (i % 4);
+    else return t * T + i;
 }
 
 __device__ __forceinline__ float epilogue(float acc, float alpha, float beta, const float* c_old) {
@@ -194,13 +178,8 @@ __global__ void __launch_bounds__(256, 2) simt_gemm_kernel(const Params p) {
     const int first_m = group * GROUP_M;
     const int gsz = min(p.tiles_m - first_m, GROUP_M);
     const int in_group = tile - group * per_group;
-    const int tm = first_m + in_group % gsz;
-    const int tn = in_group / gsz;
-
-    const int BM = RT * p.wgr;
-    const int BN = CT * p.wgc;
-    const int m0 = tm * BM;
-    const int n0 = tn * BN;
+    const int m0 = (first_m + in_group % gsz) << p.log_bm;
+    const int n0 = (in_group / gsz) << p.log_bn;
     const int64_t bz = blockIdx.z;
     const float* __restrict__ A = p.A + bz * p.sa;
     const float* __restrict__ B = p.B + bz * p.sb;
@@ -210,24 +189,22 @@ __global__ void __launch_bounds__(256, 2) simt_gemm_kernel(const Params p) {
     float* sB = smem + p.stages * p.a_elems;
     const int KT = (p.K + BK - 1) >> LOG_BK;
 
-    // A: k-contiguous rows of m (normal) or m-contiguous rows of k (TA);
-    // B: n-contiguous rows of k (normal) or k-contiguous rows of n (TB).
     auto issue = [&](int kt, int stage) {
         const int k0 = kt << LOG_BK;
         float* a_dst = sA + stage * p.a_elems;
         float* b_dst = sB + stage * p.b_elems;
-        if constexpr (!TA)
-            copy_stage<true>(a_dst, p.a_stride, A + (int64_t)m0 * p.lda, p.lda, BM, LOG_BK,
-                             p.M - m0, k0, p.K, p.vecA, tid, nthr);
-        else
-            copy_stage<false>(a_dst, p.a_stride, A + m0, p.lda, BK, p.log_bm, p.M - m0, k0, p.K,
-                              p.vecA, tid, nthr);
-        if constexpr (!TB)
-            copy_stage<false>(b_dst, p.b_stride, B + n0, p.ldb, BK, p.log_bn, p.N - n0, k0, p.K,
-                              p.vecB, tid, nthr);
-        else
-            copy_stage<true>(b_dst, p.b_stride, B + (int64_t)n0 * p.ldb, p.ldb, BN, LOG_BK,
-                             p.N - n0, k0, p.K, p.vecB, tid, nthr);
+        if constexpr (TA)   // A stored k x m: rows are K
+            copy_direct(a_dst, p.a_stride, A + (int64_t)k0 * p.lda + m0, p.lda, p.log_bm,
+                        p.M - m0, p.K - k0, p.vecA, tid, nthr);
+        else                // A stored m x k: transpose to K-major
+            copy_transpose(a_dst, p.a_stride, A + (int64_t)m0 * p.lda + k0, p.lda, p.log_bm,
+                           p.M - m0, p.K - k0, tid, nthr);
+        if constexpr (!TB)  // B stored k x n: rows are K
+            copy_direct(b_dst, p.b_stride, B + (int64_t)k0 * p.ldb + n0, p.ldb, p.log_bn,
+                        p.N - n0, p.K - k0, p.vecB, tid, nthr);
+        else                // B stored n x k: transpose to K-major
+            copy_transpose(b_dst, p.b_stride, B + (int64_t)n0 * p.ldb + k0, p.ldb, p.log_bn,
+                           p.N - n0, p.K - k0, tid, nthr);
     };
 
     float acc[RT][CT];
@@ -254,53 +231,19 @@ __global__ void __launch_bounds__(256, 2) simt_gemm_kernel(const Params p) {
         rd = (rd + 1 == S) ? 0 : rd + 1;
 #pragma unroll
         for (int kb = 0; kb < BK; kb += ACC) {
-            float a[RT][ACC];
+            float a[ACC][RT];
             float b[ACC][CT];
-            if constexpr (!TA) {
 #pragma unroll
-                for (int i = 0; i < RT; ++i)
-                    lds<ACC>(a_s + (ty + i * p.wgr) * p.a_stride + kb, a[i]);
-            } else {
-#pragma unroll
-                for (int kk = 0; kk < ACC; ++kk) {
-                    float t[RT];
-                    if constexpr (RT >= 4) {
-#pragma unroll
-                        for (int q = 0; q < RT / 4; ++q)
-                            lds<4>(a_s + (kb + kk) * p.a_stride + q * 4 * p.wgr + ty * 4, t + 4 * q);
-                    } else {
-                        lds<RT>(a_s + (kb + kk) * p.a_stride + ty * RT, t);
-                    }
-#pragma unroll
-                    for (int i = 0; i < RT; ++i) a[i][kk] = t[i];
-                }
-            }
-            if constexpr (!TB) {
-#pragma unroll
-                for (int kk = 0; kk < ACC; ++kk) {
-                    if constexpr (CT >= 4) {
-#pragma unroll
-                        for (int q = 0; q < CT / 4; ++q)
-                            lds<4>(b_s + (kb + kk) * p.b_stride + q * 4 * p.wgc + tx * 4, b[kk] + 4 * q);
-                    } else {
-                        lds<CT>(b_s + (kb + kk) * p.b_stride + tx * CT, b[kk]);
-                    }
-                }
-            } else {
-#pragma unroll
-                for (int j = 0; j < CT; ++j) {
-                    float t[ACC];
-                    lds<ACC>(b_s + (tx + j * p.wgc) * p.b_stride + kb, t);
-#pragma unroll
-                    for (int kk = 0; kk < ACC; ++kk) b[kk][j] = t[kk];
-                }
+            for (int kk = 0; kk < ACC; ++kk) {
+                load_frag<RT>(a_s + (kb + kk) * p.a_stride, ty, p.wgr, a[kk]);
+                load_frag<CT>(b_s + (kb + kk) * p.b_stride, tx, p.wgc, b[kk]);
             }
 #pragma unroll
             for (int kk = 0; kk < ACC; ++kk)
 #pragma unroll
                 for (int i = 0; i < RT; ++i)
 #pragma unroll
-                    for (int j = 0; j < CT; ++j) acc[i][j] = fmaf(a[i][kk], b[kk][j], acc[i][j]);
+                    for (int j = 0; j < CT; ++j) acc[i][j] = fmaf(a[kk][i], b[kk][j], acc[i][j]);
         }
     }
     cp_async_wait<0>();
@@ -308,10 +251,10 @@ __global__ void __launch_bounds__(256, 2) simt_gemm_kernel(const Params p) {
     // epilogue: C = alpha*acc (+ beta*C)
 #pragma unroll
     for (int i = 0; i < RT; ++i) {
-        const int m = m0 + row_of<TA, RT>(i, ty, p.wgr);
+        const int m = m0 + frag_index<RT>(i, ty, p.wgr);
         if (m >= p.M) continue;
         float* crow = C + (int64_t)m * p.ldc;
-        if constexpr (!TB && CT >= 4) {
+        if constexpr (CT >= 4) {
 #pragma unroll
             for (int q = 0; q < CT / 4; ++q) {
                 const int n = n0 + q * 4 * p.wgc + tx * 4;
@@ -338,7 +281,7 @@ __global__ void __launch_bounds__(256, 2) simt_gemm_kernel(const Params p) {
         } else {
 #pragma unroll
             for (int j = 0; j < CT; ++j) {
-                const int n = n0 + col_of<TB, CT>(j, tx, p.wgc);
+                const int n = n0 + frag_index<CT>(j, tx, p.wgc);
                 if (n < p.N) crow[n] = epilogue(acc[i][j], p.alpha, p.beta, crow + n);
             }
         }
@@ -352,19 +295,18 @@ inline int ilog2(int v) {
 }
 inline int round4(int v) { return (v + 3) & ~3; }
 
-// Shared-memory plan for one (layout, tile) combination; used by the
-// launcher and by tests through kp_simt_smem_bytes().
+// Shared-memory plan for one tile shape (both operands K-major).
 struct SmemPlan {
     int a_stride, b_stride, a_elems, b_elems, stages;
     size_t bytes;
 };
 
-inline SmemPlan plan_smem(bool ta, bool tb, int bm, int bn) {
+inline SmemPlan plan_smem(int bm, int bn) {
     SmemPlan s;
-    if (!ta) { s.a_stride = BK + PAD; s.a_elems = bm * s.a_stride; }
-    else     { s.a_stride = round4(bm) + PAD; s.a_elems = BK * s.a_stride; }
-    if (!tb) { s.b_stride = round4(bn) + PAD; s.b_elems = BK * s.b_stride; }
-    else     { s.b_stride = BK + PAD; s.b_elems = bn * s.b_stride; }
+    s.a_stride = round4(bm) + PAD;
+    s.b_stride = round4(bn) + PAD;
+    s.a_elems = BK * s.a_stride;
+    s.b_elems = BK * s.b_stride;
     const size_t stage = 4u * size_t(s.a_elems + s.b_elems);
     s.stages = (3 * stage <= 112 * 1024) ? 3 : 2;
     s.bytes = s.stages * stage;
@@ -374,10 +316,10 @@ inline SmemPlan plan_smem(bool ta, bool tb, int bm, int bn) {
 template <int ACC, int RT, int CT, bool TA, bool TB>
 kp_status launch(const GemmProblem& g, int wgr, int wgc, cudaStream_t stream) {
     const int bm = RT * wgr, bn = CT * wgc;
-    const SmemPlan sp = plan_smem(TA, TB, bm, bn);
+    const SmemPlan sp = plan_smem(bm, bn);
     if (sp.bytes > 227 * 1024) return fail(KP_ERR_UNSUPPORTED, "simt: shared-memory plan too large");
     auto kern = simt_gemm_kernel<ACC, RT, CT, TA, TB>;
-    static bool attr_done = false;  // benign race: idempotent attribute set
+    static bool attr_done = false;  // idempotent; one process drives one device
     if (!attr_done) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
             return check_launch("cudaFuncSetAttribute");
@@ -395,8 +337,9 @@ kp_status launch(const GemmProblem& g, int wgr, int wgc, cudaStream_t stream) {
     p.log_bm = ilog2(bm); p.log_bn = ilog2(bn);
     p.stages = sp.stages;
     const bool multi = g.batch > 1;
-    p.vecA = aligned16(g.A) && g.lda % 4 == 0 && (!multi || g.sa % 4 == 0) && (!TA || bm % 4 == 0);
-    p.vecB = aligned16(g.B) && g.ldb % 4 == 0 && (!multi || g.sb % 4 == 0) && (TB || bn % 4 == 0);
+    // 16-byte copies need 16-byte aligned rows of the m/n-contiguous operands
+    p.vecA = TA && aligned16(g.A) && g.lda % 4 == 0 && (!multi || g.sa % 4 == 0) && bm % 4 == 0;
+    p.vecB = !TB && aligned16(g.B) && g.ldb % 4 == 0 && (!multi || g.sb % 4 == 0) && bn % 4 == 0;
     p.vecC = aligned16(g.C) && g.ldc % 4 == 0 && (!multi || g.sc % 4 == 0);
     p.tiles_m = int((g.m + bm - 1) / bm);
     p.tiles_n = int((g.n + bn - 1) / bn);

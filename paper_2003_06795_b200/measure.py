@@ -166,6 +166,32 @@ def merge_shards(n_problems: int, n_configs: int, parts) -> np.ndarray:
     return grid
 
 
+def config_shard(n_configs: int, rank: int, world: int) -> list[int]:
+    """Interleaved config shard of one rank (bench.py under torchrun): config
+    costs vary smoothly along the canonical order, so striding balances."""
+    if not 0 <= rank < world:
+        raise ValueError("rank out of range")
+    return list(range(rank, n_configs, world))
+
+
+def gather_cells(local: dict, world: int, group=None) -> dict:
+    """Merge every rank's {(problem, config): runtime_ns} on all ranks with a
+    host-side object all-gather (gloo group); a cell measured twice is an
+    error. No device-to-device traffic: the sweep has no data exchange."""
+    if world == 1:
+        return dict(local)
+    import torch.distributed as dist
+    parts = [None] * world
+    dist.all_gather_object(parts, local, group=group)
+    merged: dict = {}
+    for part in parts:
+        for key, val in part.items():
+            if key in merged:
+                raise RuntimeError(f"cell {key} measured by two ranks")
+            merged[key] = val
+    return merged
+
+
 def _worker(device: int, spec: SweepSpec, task_q, result_q) -> None:
     """One process per GPU: pull problem indices until the queue is empty."""
     os.environ["CUDA_VISIBLE_DEVICES"] = str(device)

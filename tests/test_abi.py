@@ -1,0 +1,101 @@
+"""The C-ABI library (libkp.so) loads without a GPU and exports every symbol
+include/kp_abi.h declares; config enumeration and argument validation work
+host-side (no compute call is made here)."""
+
+import ctypes
+import re
+from pathlib import Path
+
+import pytest
+
+from paper_2003_06795_b200 import _native as nat
+from paper_2003_06795_b200 import dataset
+
+HEADER = Path(__file__).resolve().parents[1] / "include" / "kp_abi.h"
+
+
+def declared_symbols():
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"\b(kp_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_declares_what_binding_expects():
+    assert sorted(nat.EXPORTS) == declared_symbols()
+
+
+def test_library_exports_every_declared_symbol():
+    lib = nat.lib()
+    for name in declared_symbols():
+        assert hasattr(lib, name), name
+    assert lib.kp_abi_version() == 1
+
+
+def test_config_space_matches_reference_order():
+    lib = nat.lib()
+    assert lib.kp_num_configs(nat.F32_SIMT) == 640
+    cfg = nat.KpConfig()
+    for i, want in enumerate(dataset.all_configs()):
+        assert lib.kp_config_at(nat.F32_SIMT, i, ctypes.byref(cfg)) == nat.KP_OK
+        assert cfg.as_tuple() == want.as_tuple()
+    assert lib.kp_config_at(nat.F32_SIMT, 640, ctypes.byref(cfg)) == nat.KP_ERR_INVALID_ARG
+
+
+@pytest.mark.parametrize("bad", [(3, 4, 4, 8, 8), (4, 16, 4, 8, 8), (4, 4, 4, 4, 4),
+                                 (0, 1, 1, 1, 64)])
+def test_invalid_config_status(bad):
+    lib = nat.lib()
+    assert lib.kp_config_valid(nat.F32_SIMT, nat.KpConfig(*bad)) == nat.KP_ERR_INVALID_CONFIG
+    assert b"domain" in lib.kp_last_error()
+
+
+def _desc(**kw):
+    d = dict(batch=1, m=4, k=4, n=4, trans_a=0, trans_b=0, lda=4, ldb=4, ldc=4, stride_a=0,
+             stride_b=0, stride_c=16, alpha=1.0, beta=0.0)
+    d.update(kw)
+    return nat.KpGemmDesc(**d)
+
+
+@pytest.mark.parametrize("kw,status", [
+    (dict(m=0), nat.KP_ERR_BAD_SHAPE), (dict(k=-1), nat.KP_ERR_BAD_SHAPE),
+    (dict(lda=3), nat.KP_ERR_BAD_SHAPE), (dict(ldb=2), nat.KP_ERR_BAD_SHAPE),
+    (dict(ldc=1), nat.KP_ERR_BAD_SHAPE), (dict(batch=2, stride_c=3), nat.KP_ERR_BAD_SHAPE),
+])
+def test_shape_validation_before_any_launch(kw, status):
+    lib = nat.lib()
+    d = _desc(**kw)
+    buf = ctypes.c_void_p(16)  # never dereferenced: validation fails first
+    rc = lib.kp_gemm(nat.F32_SIMT, nat.KpConfig(4, 4, 4, 8, 8), ctypes.byref(d), buf, buf, buf, None)
+    assert rc == status
+    with pytest.raises(dataset.DataError):
+        nat.check(rc, "kp_gemm")
+
+
+def test_null_pointers_rejected():
+    lib = nat.lib()
+    d = _desc()
+    assert lib.kp_gemm(nat.F32_SIMT, nat.KpConfig(4, 4, 4, 8, 8), ctypes.byref(d), None, None,
+                       None, None) == nat.KP_ERR_INVALID_ARG
+
+
+def test_selector_table_consistent():
+    """kp_select answers from the compiled generated headers, or reports
+    UNSUPPORTED for variants without one; answers are valid configs."""
+    from paper_2003_06795_b200 import libgen
+    lib = nat.lib()
+    installed = set(libgen.installed())
+    cfg = nat.KpConfig()
+    for fam, fid in nat.FAMILIES.items():
+        for trans in libgen.TRANS:
+            rc = lib.kp_select(fid, int(trans[0] == "t"), int(trans[1] == "t"), 256, 256, 256,
+                               ctypes.byref(cfg))
+            if (fam, trans) in installed:
+                assert rc == nat.KP_OK
+                assert lib.kp_config_valid(fid, cfg) == nat.KP_OK
+            else:
+                assert rc == nat.KP_ERR_UNSUPPORTED
+
+
+def test_status_strings():
+    lib = nat.lib()
+    for st in range(7):
+        assert lib.kp_status_string(st)

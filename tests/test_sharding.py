@@ -1,0 +1,82 @@
+"""Multi-GPU sweep plumbing on CPU: shard planning, merging, and the
+world_size-2 gloo gather used by bench.py (no GPU, no data-path collective)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from paper_2003_06795_b200 import measure, shapes
+from paper_2003_06795_b200.dataset import ProblemSize
+
+
+def test_plan_shards_partitions_and_balances():
+    probs = shapes.problem_set("networks")
+    for n in (1, 2, 4, 8):
+        shards = measure.plan_shards(probs, n)
+        flat = sorted(i for s in shards for i in s)
+        assert flat == list(range(len(probs)))
+        loads = [sum(measure.problem_cost(probs[i]) for i in s) for s in shards]
+        if n > 1:
+            # LPT bound: max load <= mean + largest single task
+            assert max(loads) <= sum(loads) / n + max(measure.problem_cost(p) for p in probs)
+
+
+def test_merge_shards_complete_grid():
+    parts = [{0: [1.0, 2.0], 2: [3.0, 4.0]}, {1: [5.0, 6.0]}]
+    grid = measure.merge_shards(3, 2, parts)
+    assert grid.tolist() == [[1.0, 2.0], [5.0, 6.0], [3.0, 4.0]]
+    with pytest.raises(RuntimeError):
+        measure.merge_shards(3, 2, [{0: [1.0, 1.0]}])           # missing problems
+    with pytest.raises(RuntimeError):
+        measure.merge_shards(1, 2, [{0: [1.0, 1.0]}, {0: [1.0, 1.0]}])  # duplicate
+    with pytest.raises(RuntimeError):
+        measure.merge_shards(1, 2, [{0: [1.0, float("nan")]}])  # never impute
+
+
+def test_config_shard_covers_space():
+    for world in (1, 2, 3, 8):
+        got = sorted(j for r in range(world) for j in measure.config_shard(640, r, world))
+        assert got == list(range(640))
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _gather_worker(rank, world, port, out):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    mine = measure.config_shard(10, rank, world)
+    local = {(p, j): float(100 * p + j) for p in range(3) for j in mine}
+    merged = measure.gather_cells(local, world)
+    out[rank] = sorted(merged.items())
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_gather_cells():
+    world = 2
+    port = _free_port()
+    manager = mp.Manager()
+    out = manager.dict()
+    mp.spawn(_gather_worker, args=(world, port, out), nprocs=world, join=True)
+    want = sorted(((p, j), float(100 * p + j)) for p in range(3) for j in range(10))
+    assert out[0] == want and out[1] == want
+
+
+def test_sweep_records_canonical_order():
+    spec = measure.SweepSpec((ProblemSize(2, 3, 4), ProblemSize(5, 6, 7)))
+    from paper_2003_06795_b200.dataset import all_configs
+    cfgs = all_configs()[:3]
+    rt = np.array([[10.0, 20.0, 40.0], [1.0, 2.0, 4.0]])
+    res = measure.SweepResult(spec, cfgs, rt, 1.0)
+    recs = res.records()
+    assert [r.problem.as_tuple() for r in recs] == [(2, 3, 4)] * 3 + [(5, 6, 7)] * 3
+    assert [r.config for r in recs] == list(cfgs) * 2
+    assert recs[0].gflops == pytest.approx(2 * 2 * 3 * 4 / 10.0)
+    assert recs[0].runtime_ns == pytest.approx(10.0)
