@@ -1,17 +1,434 @@
-// K2/K3 tcgen05 families -- placeholder until the tensor-core path lands.
+// K2 / K3: tcgen05 tensor-core GEMM families (TF32 and BF16 inputs, FP32
+// accumulate in TMEM, FP32 output), same C = alpha*op(A)@op(B) + beta*C
+// contract and operand layouts as K1.
+//
+// Kernel anatomy (one 128 x BN output tile per CTA, 6 warps):
+//   warp 0  TMA producer: per stage one K slice of 128 bytes per row
+//           (32 tf32 / 64 bf16), A 128 x 128 B and B BN x 128 B, SWIZZLE_128B,
+//           zero fill for M/N/K tails, 3-D maps so batches never bleed;
+//   warp 1  TMEM allocator + single-thread tcgen05.mma issuer
+//           (M=128, N=BN, K=8 tf32 / 16 bf16 per instruction), tcgen05.commit
+//           releases the stage and finally signals the epilogue;
+//   warps 2-5 epilogue: tcgen05.ld 32x32b.x32 of their TMEM lane quarter,
+//           transpose through padded shared memory, coalesced fp32 stores
+//           with alpha/beta and bounds checks.
+// K-major operands (A normal, B transposed) and MN-major operands (A
+// transposed, B normal) differ only in the TMA box and the UMMA descriptor
+// (K-major: rows of 128 B, SBO 1024; MN-major: 128-byte MN atoms of 8 K rows,
+// LBO = BK*128, SBO = 1024), so all four layouts run without a transpose.
+//
+// Config encoding into the reference's 5-field KernelConfig:
+//   col_tile 1,2,4,8  -> BN = 32, 64, 128, 256 (UMMA N, TMEM columns)
+//   acc      1,2,4,8  -> pipeline stages 2, 3, 4, 6 (clamped to shared memory)
+//   row_tile 1        -> BM = 128 (cta_group::1)
+//   wg       (8, 8)   -> one tile per CTA, grouped raster
+// 16 configs per family, canonical KernelConfig order.
+#include <cuda.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+
 #include "tc_registry.h"
 
 namespace kp {
 namespace tc {
-int32_t num_configs(kp_family) { return 0; }
-kp_status config_at(kp_family, int32_t, kp_config*) {
-    return fail(KP_ERR_UNSUPPORTED, "tcgen05 families not built");
+
+constexpr int BM = 128;
+constexpr int NUM_THREADS = 192;
+constexpr int GROUP_M = 8;
+constexpr int STAGE_ALIGN = 1024;
+constexpr int EPI_PITCH = 33;  // padded 32x32 staging tile per epilogue warp
+
+struct TcParams {
+    float* C;
+    int M, N, K;
+    int64_t ldc, sc;
+    float alpha, beta;
+    int tiles_m, tiles_n;
+    int stages, k_tiles;
+    int a_batch, b_batch;  // 1 if the operand advances with the batch index, else 0
+};
+
+// ------------------------------------------------------------ PTX wrappers
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(bar), "r"(count) : "memory");
 }
-kp_status valid(kp_family, const kp_config&) {
-    return fail(KP_ERR_UNSUPPORTED, "tcgen05 families not built");
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                 :: "r"(bar), "r"(bytes) : "memory");
 }
-kp_status launch(kp_family, const kp_config&, const GemmProblem&, cudaStream_t) {
-    return fail(KP_ERR_UNSUPPORTED, "tcgen05 families not built");
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra DONE_%=;\n\t"
+        "bra WAIT_%=;\n\t"
+        "DONE_%=:\n\t}" :: "r"(bar), "r"(parity) : "memory");
 }
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];"
+        :: "r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                 :: "r"(bar) : "memory");
+}
+__device__ __forceinline__ void fence_after_sync() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void fence_before_sync() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+
+// UMMA shared-memory descriptor (SWIZZLE_128B, Blackwell version bits = 1).
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= uint64_t((addr >> 4) & 0x3FFF);
+    d |= uint64_t((lbo >> 4) & 0x3FFF) << 16;
+    d |= uint64_t((sbo >> 4) & 0x3FFF) << 32;
+    d |= uint64_t(1) << 46;  // descriptor version (sm_100)
+    d |= uint64_t(2) << 61;  // layout type: SWIZZLE_128B
+    return d;
+}
+
+template <int ES, bool A_MN, bool B_MN, int BN>
+__host__ __device__ constexpr uint32_t instr_desc() {
+    // c_format F32 (bit 4), a/b format (bits 7-9 / 10-12): bf16 = 1, tf32 = 2,
+    // a/b major (bits 15/16), N >> 3 (bits 17-22), M >> 4 (bits 24-28)
+    return (1u << 4) | ((ES == 4 ? 2u : 1u) << 7) | ((ES == 4 ? 2u : 1u) << 10) |
+           (uint32_t(A_MN) << 15) | (uint32_t(B_MN) << 16) | (uint32_t(BN >> 3) << 17) |
+           (uint32_t(BM >> 4) << 24);
+}
+
+template <int ES>
+__device__ __forceinline__ void mma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                    uint32_t accumulate) {
+    if constexpr (ES == 4) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
+            :: "r"(tmem_d), "l"(a), "l"(b), "r"(idesc), "r"(accumulate) : "memory");
+    } else {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+            :: "r"(tmem_d), "l"(a), "l"(b), "r"(idesc), "r"(accumulate) : "memory");
+    }
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+        "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+          "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+          "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+          "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// ------------------------------------------------------------------ kernel
+template <int ES, int BN, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+               const TcParams p) {
+    constexpr int ROW = 128;                  // bytes of K per operand row per stage
+    constexpr int BK = ROW / ES;              // K elements per stage
+    constexpr int UMMA_K = 32 / ES;           // K per tcgen05.mma
+    constexpr int MN_ATOM = ROW / ES;         // MN elements per 128-byte MN-major atom
+    constexpr uint32_t A_BYTES = BM * ROW;
+    constexpr uint32_t B_BYTES = BN * ROW;
+    constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+    constexpr uint32_t IDESC = instr_desc<ES, A_MN, B_MN, BN>();
+
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // 1024-byte aligned stage ring, then barriers, TMEM slot, epilogue staging
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + STAGE_ALIGN - 1) & ~uint32_t(STAGE_ALIGN - 1);
+    uint8_t* gbase = smem_raw + (base - raw);
+    const int S = p.stages;
+    const uint32_t bars = base + S * STAGE_BYTES;              // full[S], empty[S], done
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + S * STAGE_BYTES + (2 * S + 1) * 8);
+    float* staging = reinterpret_cast<float*>(gbase + S * STAGE_BYTES + (2 * S + 2) * 8);
+    auto full_bar = [&](int s) { return bars + 8u * s; };
+    auto empty_bar = [&](int s) { return bars + 8u * (S + s); };
+    const uint32_t done_bar = bars + 8u * (2 * S);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+
+    const int tile = blockIdx.x;
+    const int per_group = GROUP_M * p.tiles_n;
+    const int group = tile / per_group;
+    const int first_m = group * GROUP_M;
+    const int gsz = min(p.tiles_m - first_m, GROUP_M);
+    const int in_group = tile - group * per_group;
+    const int m0 = (first_m + in_group % gsz) * BM;
+    const int n0 = (in_group / gsz) * BN;
+    const int bz = blockIdx.z;
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(full_bar(s), 1);
+            mbar_init(empty_bar(s), 1);
+        }
+        mbar_init(done_bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                     :: "r"(smem_u32(tmem_slot)), "r"(BN) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    fence_before_sync();
+    __syncthreads();
+    fence_after_sync();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---- TMA producer
+            const int za = bz * p.a_batch, zb = bz * p.b_batch;
+            for (int kt = 0; kt < p.k_tiles; ++kt) {
+                const int s = kt % S;
+                const uint32_t phase = (kt / S) & 1;
+                mbar_wait(empty_bar(s), phase ^ 1);
+                mbar_expect_tx(full_bar(s), STAGE_BYTES);
+                const uint32_t sa = base + s * STAGE_BYTES;
+                const uint32_t sb = sa + A_BYTES;
+                const int k0 = kt * BK;
+                if constexpr (!A_MN) {
+                    tma_load_3d(sa, &map_a, k0, m0, za, full_bar(s));
+                } else {
+#pragma unroll
+                    for (int j = 0; j < BM / MN_ATOM; ++j)
+                        tma_load_3d(sa + j * BK * ROW, &map_a, m0 + j * MN_ATOM, k0, za, full_bar(s));
+                }
+                if constexpr (!B_MN) {
+                    tma_load_3d(sb, &map_b, k0, n0, zb, full_bar(s));
+                } else {
+#pragma unroll
+                    for (int j = 0; j < BN / MN_ATOM; ++j)
+                        tma_load_3d(sb + j * BK * ROW, &map_b, n0 + j * MN_ATOM, k0, zb, full_bar(s));
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---- MMA issuer
+            for (int kt = 0; kt < p.k_tiles; ++kt) {
+                const int s = kt % S;
+                const uint32_t phase = (kt / S) & 1;
+                mbar_wait(full_bar(s), phase);
+                fence_after_sync();
+                const uint32_t sa = base + s * STAGE_BYTES;
+                const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+                for (int k = 0; k < BK / UMMA_K; ++k) {
+                    // K-major: advance 32 B inside the swizzled row; MN-major:
+                    // advance UMMA_K/8 groups of 8 K rows (1024 B each)
+                    const uint64_t da = A_MN ? smem_desc(sa + k * (UMMA_K / 8) * 1024, BK * ROW, 1024)
+                                             : smem_desc(sa + k * 32, 16, 1024);
+                    const uint64_t db = B_MN ? smem_desc(sb + k * (UMMA_K / 8) * 1024, BK * ROW, 1024)
+                                             : smem_desc(sb + k * 32, 16, 1024);
+                    mma<ES>(tmem, da, db, IDESC, (kt | k) != 0);
+                }
+                umma_commit(empty_bar(s));  // frees the stage once these MMAs retire
+            }
+            umma_commit(done_bar);          // accumulator complete
+        }
+    } else {  // ---- epilogue warps 2..5: TMEM lane quarter = warp % 4
+        const int q = warp & 3;
+        float* st = staging + (warp - 2) * 32 * EPI_PITCH;
+        mbar_wait(done_bar, 0);
+        fence_after_sync();
+        float* Cb = p.C + int64_t(bz) * p.sc;
+        const int row0 = m0 + q * 32;
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+            float v[32];
+            tmem_ld32(tmem + (uint32_t(q * 32) << 16) + c0, v);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) st[lane * EPI_PITCH + j] = v[j];
+            __syncwarp();
+            const int n = n0 + c0 + lane;
+            if (n < p.N) {
+#pragma unroll 4
+                for (int r = 0; r < 32; ++r) {
+                    const int m = row0 + r;
+                    if (m < p.M) {
+                        float* dst = Cb + int64_t(m) * p.ldc + n;
+                        const float x = p.alpha * st[r * EPI_PITCH + lane];
+                        *dst = p.beta == 0.0f ? x : fmaf(p.beta, *dst, x);
+                    }
+                }
+            }
+            __syncwarp();
+        }
+    }
+    fence_before_sync();
+    __syncthreads();
+    if (warp == 1) {
+        fence_after_sync();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(BN)
+                     : "memory");
+    }
+}
+
+// ------------------------------------------------------------------- host
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeFn encoder() {
+    static EncodeFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+                cudaSuccess && q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(ptr);
+    });
+    return fn;
+}
+
+// 3-D tensor map over (inner, outer, batch) with a 128-byte swizzled box.
+static kp_status make_map(CUtensorMap* map, bool bf16, const void* ptr, int64_t inner,
+                          int64_t outer, int64_t batch, int64_t ld, int64_t bstride, int box_inner,
+                          int box_outer) {
+    EncodeFn enc = encoder();
+    if (!enc) return fail(KP_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
+    const int es = bf16 ? 2 : 4;
+    cuuint64_t dims[3] = {cuuint64_t(inner), cuuint64_t(outer), cuuint64_t(batch)};
+    cuuint64_t strides[2] = {cuuint64_t(ld * es), cuuint64_t((batch > 1 ? bstride : outer * ld) * es)};
+    cuuint32_t box[3] = {cuuint32_t(box_inner), cuuint32_t(box_outer), 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = enc(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                           3, const_cast<void*>(ptr), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(KP_ERR_ALIGNMENT, "cuTensorMapEncodeTiled rejected the operand");
+    return KP_OK;
+}
+
+static const uint32_t kTiles[4] = {1, 2, 4, 8};
+static int tidx(uint32_t v) {
+    for (int i = 0; i < 4; ++i)
+        if (kTiles[i] == v) return i;
+    return -1;
+}
+
+int32_t num_configs(kp_family fam) { return (fam == KP_TF32_TC || fam == KP_BF16_TC) ? 16 : 0; }
+
+kp_status config_at(kp_family fam, int32_t index, kp_config* out) {
+    if (index < 0 || index >= num_configs(fam)) return fail(KP_ERR_INVALID_ARG, "config index out of range");
+    *out = kp_config{kTiles[index / 4], 1u, kTiles[index % 4], 8u, 8u};
+    return KP_OK;
+}
+
+kp_status valid(kp_family fam, const kp_config& c) {
+    if (num_configs(fam) == 0) return fail(KP_ERR_INVALID_ARG, "not a tensor-core family");
+    if (tidx(c.acc) < 0 || c.row_tile != 1 || tidx(c.col_tile) < 0 || c.wg_rows != 8 || c.wg_cols != 8)
+        return fail(KP_ERR_INVALID_CONFIG,
+                    "tcgen05 family configs are (acc in 1,2,4,8; row_tile 1; col_tile in 1,2,4,8; wg 8x8)");
+    return KP_OK;
+}
+
+static size_t smem_bytes(int bn, int stages) {
+    return STAGE_ALIGN + size_t(stages) * (BM + bn) * 128 + (2 * stages + 2) * 8 +
+           4 * 32 * EPI_PITCH * 4;
+}
+
+template <int ES, int BN, bool A_MN, bool B_MN>
+static kp_status launch_t(const GemmProblem& g, int want_stages, cudaStream_t stream) {
+    int stages = want_stages;
+    while (stages > 2 && smem_bytes(BN, stages) > 227 * 1024) --stages;
+    const size_t smem = smem_bytes(BN, stages);
+    const bool bf16 = ES == 2;
+    const int BK = 128 / ES, ATOM = 128 / ES;
+    CUtensorMap ma, mb;
+    kp_status st;
+    const int64_t bat_a = g.sa ? g.batch : 1, bat_b = g.sb ? g.batch : 1;
+    if (!A_MN) st = make_map(&ma, bf16, g.A, g.k, g.m, bat_a, g.lda, g.sa, BK, BM);
+    else       st = make_map(&ma, bf16, g.A, g.m, g.k, bat_a, g.lda, g.sa, ATOM, BK);
+    if (st != KP_OK) return st;
+    if (!B_MN) st = make_map(&mb, bf16, g.B, g.k, g.n, bat_b, g.ldb, g.sb, BK, BN);
+    else       st = make_map(&mb, bf16, g.B, g.n, g.k, bat_b, g.ldb, g.sb, ATOM, BK);
+    if (st != KP_OK) return st;
+    auto kern = tc_gemm_kernel<ES, BN, A_MN, B_MN>;
+    static bool attr_done = false;
+    if (!attr_done) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
+            return check_launch("cudaFuncSetAttribute");
+        attr_done = true;
+    }
+    TcParams p;
+    p.C = g.C;
+    p.M = int(g.m); p.N = int(g.n); p.K = int(g.k);
+    p.ldc = g.ldc; p.sc = g.sc;
+    p.alpha = g.alpha; p.beta = g.beta;
+    p.tiles_m = int((g.m + BM - 1) / BM);
+    p.tiles_n = int((g.n + BN - 1) / BN);
+    p.stages = stages;
+    p.k_tiles = int((g.k + BK - 1) / BK);
+    p.a_batch = g.sa ? 1 : 0;
+    p.b_batch = g.sb ? 1 : 0;
+    const int64_t tiles = int64_t(p.tiles_m) * p.tiles_n;
+    if (tiles > 0x7fffffffLL || g.batch > 65535) return fail(KP_ERR_BAD_SHAPE, "tc: grid too large");
+    kern<<<dim3(unsigned(tiles), 1, unsigned(g.batch)), NUM_THREADS, smem, stream>>>(ma, mb, p);
+    note_launch();
+    return check_launch("tc_gemm_kernel");
+}
+
+template <int ES, int BN>
+static kp_status by_layout(const GemmProblem& g, int stages, cudaStream_t s) {
+    // A normal = K-major, A transposed = MN-major; B transposed = K-major, B normal = MN-major
+    if (!g.ta && g.tb) return launch_t<ES, BN, false, false>(g, stages, s);
+    if (!g.ta && !g.tb) return launch_t<ES, BN, false, true>(g, stages, s);
+    if (g.ta && g.tb) return launch_t<ES, BN, true, false>(g, stages, s);
+    return launch_t<ES, BN, true, true>(g, stages, s);
+}
+
+template <int ES>
+static kp_status by_tile(const kp_config& c, const GemmProblem& g, cudaStream_t s) {
+    static const int kStages[4] = {2, 3, 4, 6};
+    const int stages = kStages[tidx(c.acc)];
+    switch (c.col_tile) {
+        case 1: return by_layout<ES, 32>(g, stages, s);
+        case 2: return by_layout<ES, 64>(g, stages, s);
+        case 4: return by_layout<ES, 128>(g, stages, s);
+        case 8: return by_layout<ES, 256>(g, stages, s);
+    }
+    return fail(KP_ERR_INVALID_CONFIG, "tc: bad col_tile");
+}
+
+kp_status launch(kp_family fam, const kp_config& c, const GemmProblem& g, cudaStream_t s) {
+    kp_status st = valid(fam, c);
+    if (st != KP_OK) return st;
+    const int es = fam == KP_BF16_TC ? 2 : 4;
+    auto al = [&](const void* ptr, int64_t ld, int64_t bs) {
+        return aligned16(ptr) && (ld * es) % 16 == 0 && (g.batch == 1 || (bs * es) % 16 == 0);
+    };
+    if (!al(g.A, g.lda, g.sa) || !al(g.B, g.ldb, g.sb))
+        return fail(KP_ERR_ALIGNMENT,
+                    "tcgen05 families need 16-byte aligned operands and row/batch pitches");
+    return fam == KP_BF16_TC ? by_tile<2>(c, g, s) : by_tile<4>(c, g, s);
+}
+
 }  // namespace tc
 }  // namespace kp

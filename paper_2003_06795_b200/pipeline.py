@@ -1,0 +1,121 @@
+"""Measured dataset -> pruned kernel set -> decision tree -> compiled selector.
+
+The paper's deployment flow on B200 data, using only the
+reference-API host pipeline (dataset.split, pruning.prune,
+selector_models.train_model, codegen.export_tree / emit_selector_source):
+
+    python -m paper_2003_06795_b200.pipeline \
+        --data data/b200_f32_nn_networks.csv.gz --family f32 --trans nn \
+        --method pca-kmeans --budget 8
+
+writes selectors/<family>_<trans>/{selection,model}.json + a score report,
+installs csrc/generated/select_<family>_<trans>.h, regenerates the selector
+table and (unless --no-build) rebuilds libkp.so.
+"""
+
+from __future__ import annotations
+
+import argparse
+import gzip
+import json
+import shutil
+import sys
+import tempfile
+from pathlib import Path
+
+from . import dataset, libgen, pruning, report, selector_models
+
+ROOT = Path(__file__).resolve().parent.parent
+SEL_DIR = ROOT / "selectors"
+
+
+def materialize(path) -> Path:
+    """Plain-CSV path for `path` (decompressing .gz into a temp file)."""
+    path = Path(path)
+    if path.suffix != ".gz":
+        return path
+    tmp = Path(tempfile.mkdtemp()) / path.stem
+    with gzip.open(path, "rb") as src, open(tmp, "wb") as dst:
+        shutil.copyfileobj(src, dst)
+    return tmp
+
+
+def load_matrix(path) -> dataset.PerformanceMatrix:
+    return dataset.normalize(dataset.build_matrix(dataset.load_records(materialize(path))))
+
+
+def choose(split: dataset.DataSplit, methods, budgets, seed: int):
+    """Score every (method, budget): selection ceiling and decision-tree
+    selector on the held-out side (reported; the deployed choice is fixed by
+    the caller's --method/--budget, so the test side is not used to pick)."""
+    opts = report.default_prune_options(split.train)
+    rows = []
+    for method in methods:
+        for budget in budgets:
+            sel = pruning.prune(method, split.train, budget, seed, opts)
+            model = selector_models.train_model(
+                "decision-tree", selector_models.make_labels(split.train, sel), seed)
+            rows.append({"method": method, "budget": budget,
+                         "ceiling": pruning.evaluate_selection(sel, split.test).percent,
+                         "decision_tree": selector_models.evaluate_model(model, split.test).percent})
+    return rows
+
+
+def build_selector(data, family: str, trans: str, method: str, budget: int, seed: int = 42,
+                   test_fraction: float = 0.2, out_dir: Path | None = None) -> dict:
+    matrix = load_matrix(data)
+    split = dataset.split(matrix, test_fraction, seed)
+    opts = report.default_prune_options(split.train)
+    sel = pruning.prune(method, split.train, budget, seed, opts)
+    model = selector_models.train_model(
+        "decision-tree", selector_models.make_labels(split.train, sel), seed)
+    out_dir = out_dir or SEL_DIR / f"{family}_{trans}"
+    out_dir.mkdir(parents=True, exist_ok=True)
+    pruning.save_selection(sel, split.train.configs, out_dir / "selection.json")
+    selector_models.save_model(model, out_dir / "model.json")
+    summary = {
+        "data": str(data), "family": family, "trans": trans, "method": method, "budget": budget,
+        "seed": seed, "test_fraction": test_fraction, "problems": len(matrix.problems),
+        "configs": len(matrix.configs),
+        "selected": [split.train.configs[j].as_tuple() for j in sel.config_indices],
+        "ceiling_pct": pruning.evaluate_selection(sel, split.test).percent,
+        "decision_tree_pct": selector_models.evaluate_model(model, split.test).percent,
+        "train_decision_tree_pct": selector_models.evaluate_model(model, split.train).percent,
+    }
+    (out_dir / "summary.json").write_text(json.dumps(summary, indent=2) + "\n")
+    return summary
+
+
+def main(argv=None) -> int:
+    ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
+    ap.add_argument("--data", required=True)
+    ap.add_argument("--family", default="f32", choices=tuple(libgen.FAMILY_IDS))
+    ap.add_argument("--trans", default="nn", choices=libgen.TRANS)
+    ap.add_argument("--method", default="pca-kmeans", choices=pruning.METHODS)
+    ap.add_argument("--budget", type=int, default=8)
+    ap.add_argument("--seed", type=int, default=42)
+    ap.add_argument("--survey", action="store_true", help="also score every method x budget")
+    ap.add_argument("--no-build", action="store_true")
+    args = ap.parse_args(argv)
+    summary = build_selector(args.data, args.family, args.trans, args.method, args.budget,
+                             args.seed)
+    print(json.dumps(summary, indent=2))
+    out_dir = SEL_DIR / f"{args.family}_{args.trans}"
+    if args.survey:
+        split = dataset.split(load_matrix(args.data), 0.2, args.seed)
+        rows = choose(split, ("top-count", "kmeans", "pca-kmeans", "decision-tree"),
+                      (4, 6, 8), args.seed)
+        (out_dir / "survey.json").write_text(json.dumps(rows, indent=2) + "\n")
+        for r in rows:
+            print(f"{r['method']:14s} {r['budget']:2d} ceiling {r['ceiling']:6.2f} "
+                  f"dt {r['decision_tree']:6.2f}")
+    libgen.install_model(out_dir / "model.json", args.family, args.trans)
+    libgen.write_selector_table()
+    if not args.no_build:
+        from .build import build_library
+        build_library()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
