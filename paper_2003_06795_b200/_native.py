@@ -12,7 +12,9 @@ from pathlib import Path
 
 from .errors import DataError
 
-LIB_PATH = Path(__file__).resolve().parent / "libkp.so"
+import os
+
+LIB_PATH = Path(os.environ.get("KP_LIB_PATH") or Path(__file__).resolve().parent / "libkp.so")
 
 F32_SIMT, TF32_TC, BF16_TC = 0, 1, 2
 FAMILIES = {"f32": F32_SIMT, "tf32": TF32_TC, "bf16": BF16_TC}

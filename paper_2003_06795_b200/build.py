@@ -72,9 +72,14 @@ def _compile(name, src, defines, force, verbose):
     return name, True
 
 
-def build_library(force: bool = False, verbose: bool = False, jobs: int | None = None) -> Path:
+def build_library(force: bool = False, verbose: bool = False, jobs: int | None = None,
+                  debug: bool = False) -> Path:
+    """Build libkp.so (debug=True: libkp_debug.so with -DKP_TC_DEBUG watchdog prints)."""
+    global OBJ, LIB
+    if debug:
+        OBJ, LIB = PKG / "_build_debug", PKG / "libkp_debug.so"
     OBJ.mkdir(exist_ok=True)
-    units = _units()
+    units = [(n, s, d + (["-DKP_TC_DEBUG"] if debug else [])) for n, s, d in _units()]
     jobs = jobs or max(1, os.cpu_count() or 1)
     changed = False
     with cf.ThreadPoolExecutor(max_workers=jobs) as pool:
@@ -110,8 +115,9 @@ def main(argv=None) -> int:
     ap.add_argument("--verbose", action="store_true")
     ap.add_argument("--jobs", type=int)
     ap.add_argument("--no-oracle", action="store_true")
+    ap.add_argument("--debug", action="store_true", help="libkp_debug.so (KP_TC_DEBUG)")
     args = ap.parse_args(argv)
-    lib = build_library(args.force, args.verbose, args.jobs)
+    lib = build_library(args.force, args.verbose, args.jobs, args.debug)
     print(f"built {lib}")
     if not args.no_oracle:
         print(f"built {build_oracle(args.force)}")

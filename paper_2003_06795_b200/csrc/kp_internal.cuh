@@ -36,15 +36,17 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-// 16-byte global->shared async copy; bytes beyond `src_bytes` are zero-filled.
-__device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
+// 16-byte global->shared async copy to a shared-window address; bytes beyond
+// `src_bytes` are zero-filled (src_bytes 0 reads nothing, so `src` may then
+// point anywhere).
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int src_bytes) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n"
-                 :: "r"(smem_u32(dst)), "l"(src), "r"(src_bytes) : "memory");
+                 :: "r"(dst), "l"(src), "r"(src_bytes) : "memory");
 }
-// 4-byte variant (unaligned rows, tails); src_bytes 0 writes a zero.
-__device__ __forceinline__ void cp_async4(void* dst, const void* src, int src_bytes) {
+// 4-byte variant (unaligned rows, transposes, tails); src_bytes 0 writes a zero.
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src, int src_bytes) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n"
-                 :: "r"(smem_u32(dst)), "l"(src), "r"(src_bytes) : "memory");
+                 :: "r"(dst), "l"(src), "r"(src_bytes) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() {
     asm volatile("cp.async.commit_group;\n" ::: "memory");

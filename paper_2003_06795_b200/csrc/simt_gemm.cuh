@@ -14,14 +14,15 @@
 // ("can be set at runtime and do not require additional kernels").
 //
 // B200 mapping:
-//   * shared memory holds both operands K-major (As[k][m], Bs[k][n]) with a
-//     K depth of BK = 16 per stage in a 2/3-stage cp.async ring; m/n-contiguous
-//     sources (A transposed, B normal) are copied with 16-byte cp.async,
-//     k-contiguous sources (A normal, B transposed) are transposed on the fly
-//     by 4-byte cp.async (coalesced along k, zero-filling tails);
+//   * shared memory holds both operand tiles "chunk-major" (4 output rows x
+//     BK K-slices per 16-byte-padded chunk, see chunk_off) with a K depth of
+//     BK = 16 per stage in a 2/3-stage cp.async ring; m/n-contiguous sources
+//     (A transposed, B normal) are copied with 16-byte cp.async, k-contiguous
+//     sources (A normal, B transposed) are transposed on the fly by 4-byte
+//     cp.async (coalesced along k, zero-filling tails);
 //   * a thread's rows (cols) are 4-wide chunks strided by 4*wg_rows
-//     (4*wg_cols), so every fragment read is a conflict-free LDS.128 and every
-//     C store a 16-byte STG;
+//     (4*wg_cols): every fragment read is a conflict-free LDS.128 at a
+//     per-thread base + compile-time offset, every C store a 16-byte STG;
 //   * every C element accumulates its K products in increasing k with fmaf,
 //     starting from +0, so results are bit-identical to the sequential-fmaf
 //     oracle (oracle/gemm_ref.c); K/M/N tails are zero-filled in shared memory.
@@ -34,7 +35,6 @@ namespace simt {
 
 constexpr int BK = 16;      // shared-memory K depth per pipeline stage
 constexpr int LOG_BK = 4;
-constexpr int PAD = 4;      // floats of padding per shared row (keeps 16 B alignment)
 constexpr int GROUP_M = 8;  // tile raster: 8 m-tiles share a sweep over n
 
 struct Params {
@@ -49,33 +49,46 @@ struct Params {
     int stages;
     int vecA, vecB, vecC;
     int tiles_m, tiles_n;
-    int a_stride, b_stride;  // floats per shared row (BM + pad, BN + pad)
-    int a_elems, b_elems;    // floats per stage
+    int a_elems, b_elems;    // floats per stage (chunk-major tiles)
 };
 
-// Copy a BK x cols block whose rows are K (source row pitch ld, element
-// (k, c) at src[k*ld + c], cols = 1 << log_cols) into s[k*s_stride + c].
-// Elements with k >= kv or c >= cv are written as zero.
-__device__ __forceinline__ void copy_direct(float* s, int s_stride, const float* src, int64_t ld,
-                                            int log_cols, int cv, int kv, bool vec, int tid,
-                                            int nthr) {
+// Shared-memory tile layout ("chunk-major"): an operand tile of BM (or BN)
+// rows of the output axis is stored as BM/4 chunks of 4 consecutive rows, each
+// chunk holding its BK K-slices as 16-byte float4s:
+//     element (k, m)  at  (m >> 2) * CH + k * 4 + (m & 3),   CH = BK*4 + 4.
+// A thread's 4-row fragment at slice k is one LDS.128 whose offset is a
+// per-thread base plus the compile-time k*4, so the unrolled K loop needs no
+// address arithmetic (the runtime work-group shape only enters the bases);
+// the 4-float pad per chunk makes 8 consecutive chunks hit 8 different 16-byte
+// bank groups.
+constexpr int CH = BK * 4 + 4;
+
+__device__ __forceinline__ int chunk_off(int k, int m) { return (m >> 2) * CH + k * 4 + (m & 3); }
+
+// Copy a BK x cols block whose rows are K and whose columns (the M/N axis,
+// cols = 1 << log_cols) are contiguous in global memory (element (k, c) at
+// src[k*ld + c]) into the chunk-major tile at shared address `s`. Elements
+// with k >= kv or c >= cv are written as zero. 16-byte copies when vec.
+__device__ __forceinline__ void copy_direct(uint32_t s, const float* src, int64_t ld, int log_cols,
+                                            int cv, int kv, bool vec, int tid, int nthr) {
     if (vec && log_cols >= 2) {
         const int log_cpr = log_cols - 2;
         const int total = BK << log_cpr;
         if ((nthr >> log_cpr) > 0 && total <= 8 * nthr) {
-            // fast: every chunk of this thread sits in one column, dr rows apart
+            // fast: every chunk of this thread sits in one column, dr K-rows apart
             const int r0 = tid >> log_cpr;
             const int c0 = (tid & ((1 << log_cpr) - 1)) << 2;
             const int dr = nthr >> log_cpr;
             const int n = total >= nthr ? total / nthr : (tid < total ? 1 : 0);
             const int cbytes = min(max(cv - c0, 0), 4) * 4;
             const float* gp = src + (int64_t)r0 * ld + c0;
-            float* sp = s + r0 * s_stride + c0;
+            const int64_t gstep = (int64_t)dr * ld;
+            const uint32_t sp = s + 4u * chunk_off(r0, c0);
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
                 if (c < n) {
-                    const int bytes = r0 + c * dr < kv ? cbytes : 0;
-                    cp_async16(sp + c * dr * s_stride, bytes ? gp + (int64_t)c * dr * ld : src, bytes);
+                    cp_async16(sp + c * dr * 16, gp, r0 + c * dr < kv ? cbytes : 0);
+                    gp += gstep;
                 }
             }
             return;
@@ -83,8 +96,8 @@ __device__ __forceinline__ void copy_direct(float* s, int s_stride, const float*
         for (int idx = tid; idx < total; idx += nthr) {
             const int r = idx >> log_cpr;
             const int c = (idx & ((1 << log_cpr) - 1)) << 2;
-            const int bytes = r < kv ? min(max(cv - c, 0), 4) * 4 : 0;
-            cp_async16(s + r * s_stride + c, bytes ? src + (int64_t)r * ld + c : src, bytes);
+            cp_async16(s + 4u * chunk_off(r, c), src + (int64_t)r * ld + c,
+                       r < kv ? min(max(cv - c, 0), 4) * 4 : 0);
         }
         return;
     }
@@ -92,38 +105,37 @@ __device__ __forceinline__ void copy_direct(float* s, int s_stride, const float*
     for (int idx = tid; idx < total; idx += nthr) {
         const int r = idx >> log_cols;
         const int c = idx & ((1 << log_cols) - 1);
-        const bool ok = r < kv && c < cv;
-        cp_async4(s + r * s_stride + c, ok ? src + (int64_t)r * ld + c : src, ok ? 4 : 0);
+        cp_async4(s + 4u * chunk_off(r, c), src + (int64_t)r * ld + c, (r < kv && c < cv) ? 4 : 0);
     }
 }
 
-// Transposing copy: source rows are the non-K axis (element (r, k) at
-// src[r*ld + k], rows = 1 << log_rows), destination K-major s[k*s_stride + r].
-// 4-byte cp.async with consecutive threads along k (coalesced reads); nthr is
-// a multiple of BK so each thread keeps one k and strides over rows.
-__device__ __forceinline__ void copy_transpose(float* s, int s_stride, const float* src, int64_t ld,
+// Transposing copy: the source rows are the M/N axis (element (r, k) at
+// src[r*ld + k], rows = 1 << log_rows). 4-byte cp.async with consecutive
+// threads along k (coalesced reads); nthr is a multiple of BK so each thread
+// keeps one k and strides over rows.
+__device__ __forceinline__ void copy_transpose(uint32_t s, const float* src, int64_t ld,
                                                int log_rows, int rv, int kv, int tid, int nthr) {
     const int k = tid & (BK - 1);
     const int r0 = tid >> LOG_BK;
     const int rstep = nthr >> LOG_BK;
     const int rows = 1 << log_rows;
-    const bool kin = k < kv;
-    const float* gp = src + k;
-    float* sp = s + k * s_stride;
+    const int kbytes = k < kv ? 4 : 0;
+    const float* gp = src + (int64_t)r0 * ld + k;
+    const int64_t gstep = (int64_t)rstep * ld;
     if (rows <= 16 * rstep) {
 #pragma unroll
         for (int c = 0; c < 16; ++c) {
             const int r = r0 + c * rstep;
             if (r < rows) {
-                const bool ok = kin && r < rv;
-                cp_async4(sp + r, ok ? gp + (int64_t)r * ld : src, ok ? 4 : 0);
+                cp_async4(s + 4u * chunk_off(k, r), gp, r < rv ? kbytes : 0);
+                gp += gstep;
             }
         }
         return;
     }
     for (int r = r0; r < rows; r += rstep) {
-        const bool ok = kin && r < rv;
-        cp_async4(sp + r, ok ? gp + (int64_t)r * ld : src, ok ? 4 : 0);
+        cp_async4(s + 4u * chunk_off(k, r), gp, r < rv ? kbytes : 0);
+        gp += gstep;
     }
 }
 
@@ -141,15 +153,32 @@ __device__ __forceinline__ void lds(const float* p, float* out) {
     }
 }
 
-// The T values thread `t` owns along one axis of a K-major tile row: 4-wide
-// chunks strided by 4*wg when T >= 4, else T contiguous values.
+// Thread t's fragment along one output axis: T >= 4 -> chunks q*wg + t
+// (rows q*4*wg + t*4 + e), else rows t*T + i. frag_base gives the per-thread
+// shared offsets, frag_index the output row/col of fragment element i.
 template <int T>
-__device__ __forceinline__ void load_frag(const float* row, int t, int wg, float* out) {
+struct FragBase {
+    int off[T >= 4 ? T / 4 : 1];
+};
+template <int T>
+__device__ __forceinline__ FragBase<T> frag_base(int t, int wg) {
+    FragBase<T> f;
     if constexpr (T >= 4) {
 #pragma unroll
-        for (int q = 0; q < T / 4; ++q) lds<4>(row + q * 4 * wg + t * 4, out + 4 * q);
+        for (int q = 0; q < T / 4; ++q) f.off[q] = (q * wg + t) * CH;
     } else {
-        lds<T>(row + t * T, out);
+        f.off[0] = ((t * T) >> 2) * CH + ((t * T) & 3);
+    }
+    return f;
+}
+template <int T>
+__device__ __forceinline__ void load_frag(const float* stage, const FragBase<T>& f, int k,
+                                          float* out) {
+    if constexpr (T >= 4) {
+#pragma unroll
+        for (int q = 0; q < T / 4; ++q) lds<4>(stage + f.off[q] + k * 4, out + 4 * q);
+    } else {
+        lds<T>(stage + f.off[0] + k * 4, out);
     }
 }
 template <int T>
@@ -187,26 +216,29 @@ __global__ void __launch_bounds__(256, 2) simt_gemm_kernel(const Params p) {
 
     float* sA = smem;
     float* sB = smem + p.stages * p.a_elems;
+    const uint32_t sA_u = smem_u32(sA), sB_u = smem_u32(sB);
     const int KT = (p.K + BK - 1) >> LOG_BK;
 
     auto issue = [&](int kt, int stage) {
         const int k0 = kt << LOG_BK;
-        float* a_dst = sA + stage * p.a_elems;
-        float* b_dst = sB + stage * p.b_elems;
+        const uint32_t a_dst = sA_u + 4u * stage * p.a_elems;
+        const uint32_t b_dst = sB_u + 4u * stage * p.b_elems;
         if constexpr (TA)   // A stored k x m: rows are K
-            copy_direct(a_dst, p.a_stride, A + (int64_t)k0 * p.lda + m0, p.lda, p.log_bm,
-                        p.M - m0, p.K - k0, p.vecA, tid, nthr);
-        else                // A stored m x k: transpose to K-major
-            copy_transpose(a_dst, p.a_stride, A + (int64_t)m0 * p.lda + k0, p.lda, p.log_bm,
-                           p.M - m0, p.K - k0, tid, nthr);
+            copy_direct(a_dst, A + (int64_t)k0 * p.lda + m0, p.lda, p.log_bm, p.M - m0,
+                        p.K - k0, p.vecA, tid, nthr);
+        else                // A stored m x k: transpose
+            copy_transpose(a_dst, A + (int64_t)m0 * p.lda + k0, p.lda, p.log_bm, p.M - m0,
+                           p.K - k0, tid, nthr);
         if constexpr (!TB)  // B stored k x n: rows are K
-            copy_direct(b_dst, p.b_stride, B + (int64_t)k0 * p.ldb + n0, p.ldb, p.log_bn,
-                        p.N - n0, p.K - k0, p.vecB, tid, nthr);
-        else                // B stored n x k: transpose to K-major
-            copy_transpose(b_dst, p.b_stride, B + (int64_t)n0 * p.ldb + k0, p.ldb, p.log_bn,
-                           p.N - n0, p.K - k0, tid, nthr);
+            copy_direct(b_dst, B + (int64_t)k0 * p.ldb + n0, p.ldb, p.log_bn, p.N - n0,
+                        p.K - k0, p.vecB, tid, nthr);
+        else                // B stored n x k: transpose
+            copy_transpose(b_dst, B + (int64_t)n0 * p.ldb + k0, p.ldb, p.log_bn, p.N - n0,
+                           p.K - k0, tid, nthr);
     };
 
+    const FragBase<RT> fa = frag_base<RT>(ty, p.wgr);
+    const FragBase<CT> fb = frag_base<CT>(tx, p.wgc);
     float acc[RT][CT];
 #pragma unroll
     for (int i = 0; i < RT; ++i)
@@ -235,8 +267,8 @@ __global__ void __launch_bounds__(256, 2) simt_gemm_kernel(const Params p) {
             float b[ACC][CT];
 #pragma unroll
             for (int kk = 0; kk < ACC; ++kk) {
-                load_frag<RT>(a_s + (kb + kk) * p.a_stride, ty, p.wgr, a[kk]);
-                load_frag<CT>(b_s + (kb + kk) * p.b_stride, tx, p.wgc, b[kk]);
+                load_frag<RT>(a_s, fa, kb + kk, a[kk]);
+                load_frag<CT>(b_s, fb, kb + kk, b[kk]);
             }
 #pragma unroll
             for (int kk = 0; kk < ACC; ++kk)
@@ -295,18 +327,16 @@ inline int ilog2(int v) {
 }
 inline int round4(int v) { return (v + 3) & ~3; }
 
-// Shared-memory plan for one tile shape (both operands K-major).
+// Shared-memory plan for one tile shape (chunk-major operand tiles).
 struct SmemPlan {
-    int a_stride, b_stride, a_elems, b_elems, stages;
+    int a_elems, b_elems, stages;
     size_t bytes;
 };
 
 inline SmemPlan plan_smem(int bm, int bn) {
     SmemPlan s;
-    s.a_stride = round4(bm) + PAD;
-    s.b_stride = round4(bn) + PAD;
-    s.a_elems = BK * s.a_stride;
-    s.b_elems = BK * s.b_stride;
+    s.a_elems = (round4(bm) / 4) * CH;
+    s.b_elems = (round4(bn) / 4) * CH;
     const size_t stage = 4u * size_t(s.a_elems + s.b_elems);
     s.stages = (3 * stage <= 112 * 1024) ? 3 : 2;
     s.bytes = s.stages * stage;
@@ -343,7 +373,6 @@ kp_status launch(const GemmProblem& g, int wgr, int wgc, cudaStream_t stream) {
     p.vecC = aligned16(g.C) && g.ldc % 4 == 0 && (!multi || g.sc % 4 == 0);
     p.tiles_m = int((g.m + bm - 1) / bm);
     p.tiles_n = int((g.n + bn - 1) / bn);
-    p.a_stride = sp.a_stride; p.b_stride = sp.b_stride;
     p.a_elems = sp.a_elems; p.b_elems = sp.b_elems;
     const int64_t tiles = int64_t(p.tiles_m) * p.tiles_n;
     if (tiles > 0x7fffffffLL || g.batch > 65535)

@@ -58,14 +58,29 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
                  :: "r"(bar), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+__device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
     asm volatile(
-        "{\n\t.reg .pred P1;\n\t"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-        "@P1 bra DONE_%=;\n\t"
-        "bra WAIT_%=;\n\t"
-        "DONE_%=:\n\t}" :: "r"(bar), "r"(parity) : "memory");
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
+    return ok != 0;
+}
+// Wait for the phase of parity `parity`; a watchdog (~2^34 cycles, ~8 s)
+// turns a pipeline deadlock into a trapped launch error instead of a hung GPU.
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    if (mbar_try(bar, parity)) return;
+    const long long t0 = clock64();
+    while (!mbar_try(bar, parity)) {
+        if (clock64() - t0 > (1LL << 34)) {
+#ifdef KP_TC_DEBUG
+            printf("tc watchdog: block (%d,%d) thread %d bar 0x%x parity %u\n", blockIdx.x,
+                   blockIdx.z, threadIdx.x, bar, parity);
+#endif
+            __trap();
+        }
+    }
 }
 __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
                                             int c2, uint32_t bar) {
@@ -86,16 +101,35 @@ __device__ __forceinline__ void fence_before_sync() {
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
 
-// UMMA shared-memory descriptor (SWIZZLE_128B, Blackwell version bits = 1).
-__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+// UMMA shared-memory descriptor (Blackwell version bits = 1). layout: 2 =
+// SWIZZLE_128B, 4 = SWIZZLE_64B, 1 = SWIZZLE_128B_BASE32B.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo,
+                                              uint32_t layout) {
     uint64_t d = 0;
     d |= uint64_t((addr >> 4) & 0x3FFF);
     d |= uint64_t((lbo >> 4) & 0x3FFF) << 16;
     d |= uint64_t((sbo >> 4) & 0x3FFF) << 32;
     d |= uint64_t(1) << 46;  // descriptor version (sm_100)
-    d |= uint64_t(2) << 61;  // layout type: SWIZZLE_128B
+    d |= uint64_t(layout & 7) << 61;
     return d;
 }
+
+// Shared layout of an MN-major operand tile (MN contiguous in global memory):
+// atoms W bytes wide along MN, one K row per W bytes, GROUP K rows per
+// swizzle group. TF32 must use the 32-byte-granular 128B swizzle (UMMA
+// SWIZZLE_128B_BASE32B, TMA SWIZZLE_128B_ATOM_32B); BF16 uses SWIZZLE_128B,
+// or SWIZZLE_64B when the tile is only 32 elements wide.
+template <int ES, int EXTENT>
+struct MnMajor {
+    static constexpr int W = (ES == 2 && EXTENT < 64) ? 64 : 128;  // bytes per atom row
+    static constexpr int ATOM = W / ES;                             // MN elements per atom
+    static constexpr int GROUP = ES == 4 ? 4 : 8;                   // K rows per swizzle group
+    static constexpr uint32_t SBO = GROUP * W;
+    static constexpr uint32_t LAYOUT = ES == 4 ? 1u : (W == 64 ? 4u : 2u);
+    static constexpr int TMA_SWIZZLE = ES == 4 ? int(CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)
+                                               : (W == 64 ? int(CU_TENSOR_MAP_SWIZZLE_64B)
+                                                          : int(CU_TENSOR_MAP_SWIZZLE_128B));
+};
 
 template <int ES, bool A_MN, bool B_MN, int BN>
 __host__ __device__ constexpr uint32_t instr_desc() {
@@ -148,7 +182,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     constexpr int ROW = 128;                  // bytes of K per operand row per stage
     constexpr int BK = ROW / ES;              // K elements per stage
     constexpr int UMMA_K = 32 / ES;           // K per tcgen05.mma
-    constexpr int MN_ATOM = ROW / ES;         // MN elements per 128-byte MN-major atom
+    using MA = MnMajor<ES, BM>;
+    using MB = MnMajor<ES, BN>;
     constexpr uint32_t A_BYTES = BM * ROW;
     constexpr uint32_t B_BYTES = BN * ROW;
     constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
@@ -215,15 +250,15 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                     tma_load_3d(sa, &map_a, k0, m0, za, full_bar(s));
                 } else {
 #pragma unroll
-                    for (int j = 0; j < BM / MN_ATOM; ++j)
-                        tma_load_3d(sa + j * BK * ROW, &map_a, m0 + j * MN_ATOM, k0, za, full_bar(s));
+                    for (int j = 0; j < BM / MA::ATOM; ++j)
+                        tma_load_3d(sa + j * BK * MA::W, &map_a, m0 + j * MA::ATOM, k0, za, full_bar(s));
                 }
                 if constexpr (!B_MN) {
                     tma_load_3d(sb, &map_b, k0, n0, zb, full_bar(s));
                 } else {
 #pragma unroll
-                    for (int j = 0; j < BN / MN_ATOM; ++j)
-                        tma_load_3d(sb + j * BK * ROW, &map_b, n0 + j * MN_ATOM, k0, zb, full_bar(s));
+                    for (int j = 0; j < BN / MB::ATOM; ++j)
+                        tma_load_3d(sb + j * BK * MB::W, &map_b, n0 + j * MB::ATOM, k0, zb, full_bar(s));
                 }
             }
         }
@@ -238,12 +273,15 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                 const uint32_t sb = sa + A_BYTES;
 #pragma unroll
                 for (int k = 0; k < BK / UMMA_K; ++k) {
-                    // K-major: advance 32 B inside the swizzled row; MN-major:
-                    // advance UMMA_K/8 groups of 8 K rows (1024 B each)
-                    const uint64_t da = A_MN ? smem_desc(sa + k * (UMMA_K / 8) * 1024, BK * ROW, 1024)
-                                             : smem_desc(sa + k * 32, 16, 1024);
-                    const uint64_t db = B_MN ? smem_desc(sb + k * (UMMA_K / 8) * 1024, BK * ROW, 1024)
-                                             : smem_desc(sb + k * 32, 16, 1024);
+                    // K-major: advance 32 B inside the 128B-swizzled row (8-row
+                    // groups, SBO 1024); MN-major: advance UMMA_K rows of W bytes,
+                    // LBO = one atom column block (BK rows), SBO = one swizzle group
+                    const uint64_t da =
+                        A_MN ? smem_desc(sa + k * UMMA_K * MA::W, BK * MA::W, MA::SBO, MA::LAYOUT)
+                             : smem_desc(sa + k * 32, 16, 1024, 2);
+                    const uint64_t db =
+                        B_MN ? smem_desc(sb + k * UMMA_K * MB::W, BK * MB::W, MB::SBO, MB::LAYOUT)
+                             : smem_desc(sb + k * 32, 16, 1024, 2);
                     mma<ES>(tmem, da, db, IDESC, (kt | k) != 0);
                 }
                 umma_commit(empty_bar(s));  // frees the stage once these MMAs retire
@@ -310,7 +348,7 @@ static EncodeFn encoder() {
 // 3-D tensor map over (inner, outer, batch) with a 128-byte swizzled box.
 static kp_status make_map(CUtensorMap* map, bool bf16, const void* ptr, int64_t inner,
                           int64_t outer, int64_t batch, int64_t ld, int64_t bstride, int box_inner,
-                          int box_outer) {
+                          int box_outer, int swizzle) {
     EncodeFn enc = encoder();
     if (!enc) return fail(KP_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
     const int es = bf16 ? 2 : 4;
@@ -320,7 +358,7 @@ static kp_status make_map(CUtensorMap* map, bool bf16, const void* ptr, int64_t 
     cuuint32_t estr[3] = {1, 1, 1};
     const CUresult r = enc(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                            3, const_cast<void*>(ptr), dims, strides, box, estr,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CUtensorMapSwizzle(swizzle),
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(KP_ERR_ALIGNMENT, "cuTensorMapEncodeTiled rejected the operand");
     return KP_OK;
@@ -360,15 +398,18 @@ static kp_status launch_t(const GemmProblem& g, int want_stages, cudaStream_t st
     while (stages > 2 && smem_bytes(BN, stages) > 227 * 1024) --stages;
     const size_t smem = smem_bytes(BN, stages);
     const bool bf16 = ES == 2;
-    const int BK = 128 / ES, ATOM = 128 / ES;
+    const int BK = 128 / ES;
     CUtensorMap ma, mb;
     kp_status st;
     const int64_t bat_a = g.sa ? g.batch : 1, bat_b = g.sb ? g.batch : 1;
-    if (!A_MN) st = make_map(&ma, bf16, g.A, g.k, g.m, bat_a, g.lda, g.sa, BK, BM);
-    else       st = make_map(&ma, bf16, g.A, g.m, g.k, bat_a, g.lda, g.sa, ATOM, BK);
+    using MA = MnMajor<ES, BM>;
+    using MB = MnMajor<ES, BN>;
+    const int sw128 = int(CU_TENSOR_MAP_SWIZZLE_128B);
+    if (!A_MN) st = make_map(&ma, bf16, g.A, g.k, g.m, bat_a, g.lda, g.sa, BK, BM, sw128);
+    else       st = make_map(&ma, bf16, g.A, g.m, g.k, bat_a, g.lda, g.sa, MA::ATOM, BK, MA::TMA_SWIZZLE);
     if (st != KP_OK) return st;
-    if (!B_MN) st = make_map(&mb, bf16, g.B, g.k, g.n, bat_b, g.ldb, g.sb, BK, BN);
-    else       st = make_map(&mb, bf16, g.B, g.n, g.k, bat_b, g.ldb, g.sb, ATOM, BK);
+    if (!B_MN) st = make_map(&mb, bf16, g.B, g.k, g.n, bat_b, g.ldb, g.sb, BK, BN, sw128);
+    else       st = make_map(&mb, bf16, g.B, g.n, g.k, bat_b, g.ldb, g.sb, MB::ATOM, BK, MB::TMA_SWIZZLE);
     if (st != KP_OK) return st;
     auto kern = tc_gemm_kernel<ES, BN, A_MN, B_MN>;
     static bool attr_done = false;
