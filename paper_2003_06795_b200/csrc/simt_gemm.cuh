@@ -14,15 +14,19 @@
 // ("can be set at runtime and do not require additional kernels").
 //
 // B200 mapping:
-//   * shared memory holds both operand tiles "chunk-major" (4 output rows x
-//     BK K-slices per 16-byte-padded chunk, see chunk_off) with a K depth of
-//     BK = 16 per stage in a 2/3-stage cp.async ring; m/n-contiguous sources
-//     (A transposed, B normal) are copied with 16-byte cp.async, k-contiguous
-//     sources (A normal, B transposed) are transposed on the fly by 4-byte
-//     cp.async (coalesced along k, zero-filling tails);
-//   * a thread's rows (cols) are 4-wide chunks strided by 4*wg_rows
-//     (4*wg_cols): every fragment read is a conflict-free LDS.128 at a
-//     per-thread base + compile-time offset, every C store a 16-byte STG;
+//   * shared memory keeps each operand in its global orientation, K depth
+//     BK = 16 per stage, 2/3-stage cp.async ring (16-byte copies when rows
+//     are 16-byte aligned, zero-filling 4-byte copies otherwise):
+//       m/n-contiguous sources (A transposed, B normal): "chunk" layout, 4
+//         output rows x BK K-slices per padded chunk (chunk_off); a thread
+//         owns 4-wide row chunks strided by 4*wg and reads one LDS.128 per
+//         chunk per K slice, and stores C with 16-byte STG;
+//       k-contiguous sources (A normal, B transposed): "row" layout (RS
+//         pitch); a thread owns rows t + i*wg and reads K vectors of width
+//         min(acc, 4) per row -- `acc` is the K vector width, as in the
+//         paper's kernel;
+//     every fragment address is a per-thread base plus a compile-time offset,
+//     and the 8 threads of a quarter-warp always hit 8 distinct bank groups;
 //   * every C element accumulates its K products in increasing k with fmaf,
 //     starting from +0, so results are bit-identical to the sequential-fmaf
 //     oracle (oracle/gemm_ref.c); K/M/N tails are zero-filled in shared memory.
@@ -109,36 +113,6 @@ __device__ __forceinline__ void copy_direct(uint32_t s, const float* src, int64_
     }
 }
 
-// Transposing copy: the source rows are the M/N axis (element (r, k) at
-// src[r*ld + k], rows = 1 << log_rows). 4-byte cp.async with consecutive
-// threads along k (coalesced reads); nthr is a multiple of BK so each thread
-// keeps one k and strides over rows.
-__device__ __forceinline__ void copy_transpose(uint32_t s, const float* src, int64_t ld,
-                                               int log_rows, int rv, int kv, int tid, int nthr) {
-    const int k = tid & (BK - 1);
-    const int r0 = tid >> LOG_BK;
-    const int rstep = nthr >> LOG_BK;
-    const int rows = 1 << log_rows;
-    const int kbytes = k < kv ? 4 : 0;
-    const float* gp = src + (int64_t)r0 * ld + k;
-    const int64_t gstep = (int64_t)rstep * ld;
-    if (rows <= 16 * rstep) {
-#pragma unroll
-        for (int c = 0; c < 16; ++c) {
-            const int r = r0 + c * rstep;
-            if (r < rows) {
-                cp_async4(s + 4u * chunk_off(k, r), gp, r < rv ? kbytes : 0);
-                gp += gstep;
-            }
-        }
-        return;
-    }
-    for (int r = r0; r < rows; r += rstep) {
-        cp_async4(s + 4u * chunk_off(k, r), gp, r < rv ? kbytes : 0);
-        gp += gstep;
-    }
-}
-
 // Vector shared-memory load of W consecutive floats (W in 1,2,4).
 template <int W>
 __device__ __forceinline__ void lds(const float* p, float* out) {
@@ -153,39 +127,90 @@ __device__ __forceinline__ void lds(const float* p, float* out) {
     }
 }
 
-// Thread t's fragment along one output axis: T >= 4 -> chunks q*wg + t
-// (rows q*4*wg + t*4 + e), else rows t*T + i. frag_base gives the per-thread
-// shared offsets, frag_index the output row/col of fragment element i.
-template <int T>
-struct FragBase {
-    int off[T >= 4 ? T / 4 : 1];
+// Row layout ("R") for k-contiguous sources (A normal, B transposed): the
+// tile is stored as global rows, element (k, r) at r*RS + k with RS = BK + 4,
+// filled by 16-byte cp.async along k without any transpose. A thread owns
+// rows t + i*wg, so the 8 threads of a quarter-warp read 8 consecutive rows
+// (20-float pitch -> 8 distinct 16-byte bank groups) and each fragment read is
+// a float vector of up to 4 K values of one row.
+constexpr int RS = BK + 4;
+
+__device__ __forceinline__ void copy_rows(uint32_t s, const float* src, int64_t ld, int log_rows,
+                                          int rv, int kv, bool vec, int tid, int nthr) {
+    const int rows = 1 << log_rows;
+    if (vec) {
+        const int c0 = (tid & 3) << 2;  // 4 threads per 16-float row
+        const int dr = nthr >> 2;
+        const int kbytes = min(max(kv - c0, 0), 4) * 4;
+        const float* gp = src + (int64_t)(tid >> 2) * ld + c0;
+        const int64_t gstep = (int64_t)dr * ld;
+        for (int r = tid >> 2; r < rows; r += dr) {
+            cp_async16(s + 4u * (r * RS + c0), gp, r < rv ? kbytes : 0);
+            gp += gstep;
+        }
+        return;
+    }
+    const int total = rows << LOG_BK;
+    for (int idx = tid; idx < total; idx += nthr) {
+        const int r = idx >> LOG_BK;
+        const int c = idx & (BK - 1);
+        cp_async4(s + 4u * (r * RS + c), src + (int64_t)r * ld + c, (r < rv && c < kv) ? 4 : 0);
+    }
+}
+
+// Thread t's fragment along one output axis, for a K group of ACC slices.
+//   KROW (row layout):  rows t + i*wg, ACC-wide K vectors per row.
+//   chunk layout:       T >= 4 -> chunks q*wg + t (rows q*4*wg + t*4 + e),
+//                       else rows t*T + i; one T-wide vector per K slice.
+// Offsets are per-thread bases; the K offsets are compile-time immediates.
+template <bool KROW, int T, int ACC>
+struct Frag {
+    static constexpr int NB = KROW ? T : (T >= 4 ? T / 4 : 1);
+    int off[NB];
+
+    __device__ __forceinline__ void init(int t, int wg) {
+        if constexpr (KROW) {
+#pragma unroll
+            for (int i = 0; i < T; ++i) off[i] = (t + i * wg) * RS;
+        } else if constexpr (T >= 4) {
+#pragma unroll
+            for (int q = 0; q < T / 4; ++q) off[q] = (q * wg + t) * CH;
+        } else {
+            off[0] = ((t * T) >> 2) * CH + ((t * T) & 3);
+        }
+    }
+    __device__ __forceinline__ void load(const float* stage, int kb, float (&out)[ACC][T]) const {
+        if constexpr (KROW) {
+            constexpr int V = ACC < 4 ? ACC : 4;
+#pragma unroll
+            for (int i = 0; i < T; ++i) {
+#pragma unroll
+                for (int h = 0; h < ACC / V; ++h) {
+                    float v[V];
+                    lds<V>(stage + off[i] + kb + h * V, v);
+#pragma unroll
+                    for (int e = 0; e < V; ++e) out[h * V + e][i] = v[e];
+                }
+            }
+        } else {
+#pragma unroll
+            for (int kk = 0; kk < ACC; ++kk) {
+                if constexpr (T >= 4) {
+#pragma unroll
+                    for (int q = 0; q < T / 4; ++q)
+                        lds<4>(stage + off[q] + (kb + kk) * 4, &out[kk][4 * q]);
+                } else {
+                    lds<T>(stage + off[0] + (kb + kk) * 4, &out[kk][0]);
+                }
+            }
+        }
+    }
+    __device__ __forceinline__ static int index(int i, int t, int wg) {
+        if constexpr (KROW) return t + i * wg;
+        else if constexpr (T >= 4) return (i / 4) * 4 * wg + t * 4 + (i % 4);
+        else return t * T + i;
+    }
 };
-template <int T>
-__device__ __forceinline__ FragBase<T> frag_base(int t, int wg) {
-    FragBase<T> f;
-    if constexpr (T >= 4) {
-#pragma unroll
-        for (int q = 0; q < T / 4; ++q) f.off[q] = (q * wg + t) * CH;
-    } else {
-        f.off[0] = ((t * T) >> 2) * CH + ((t * T) & 3);
-    }
-    return f;
-}
-template <int T>
-__device__ __forceinline__ void load_frag(const float* stage, const FragBase<T>& f, int k,
-                                          float* out) {
-    if constexpr (T >= 4) {
-#pragma unroll
-        for (int q = 0; q < T / 4; ++q) lds<4>(stage + f.off[q] + k * 4, out + 4 * q);
-    } else {
-        lds<T>(stage + f.off[0] + k * 4, out);
-    }
-}
-template <int T>
-__device__ __forceinline__ int frag_index(int i, int t, int wg) {
-    if constexpr (T >= 4) return (i / 4) * 4 * wg + t * 4 + (i % 4);
-    else return t * T + i;
-}
 
 __device__ __forceinline__ float epilogue(float acc, float alpha, float beta, const float* c_old) {
     const float v = alpha * acc;
@@ -226,19 +251,23 @@ __global__ void __launch_bounds__(256, 2) simt_gemm_kernel(const Params p) {
         if constexpr (TA)   // A stored k x m: rows are K
             copy_direct(a_dst, A + (int64_t)k0 * p.lda + m0, p.lda, p.log_bm, p.M - m0,
                         p.K - k0, p.vecA, tid, nthr);
-        else                // A stored m x k: transpose
-            copy_transpose(a_dst, A + (int64_t)m0 * p.lda + k0, p.lda, p.log_bm, p.M - m0,
-                           p.K - k0, tid, nthr);
+        else                // A stored m x k: k-contiguous rows, row layout
+            copy_rows(a_dst, A + (int64_t)m0 * p.lda + k0, p.lda, p.log_bm, p.M - m0, p.K - k0,
+                      p.vecA, tid, nthr);
         if constexpr (!TB)  // B stored k x n: rows are K
             copy_direct(b_dst, B + (int64_t)k0 * p.ldb + n0, p.ldb, p.log_bn, p.N - n0,
                         p.K - k0, p.vecB, tid, nthr);
-        else                // B stored n x k: transpose
-            copy_transpose(b_dst, B + (int64_t)n0 * p.ldb + k0, p.ldb, p.log_bn, p.N - n0,
-                           p.K - k0, tid, nthr);
+        else                // B stored n x k: k-contiguous rows, row layout
+            copy_rows(b_dst, B + (int64_t)n0 * p.ldb + k0, p.ldb, p.log_bn, p.N - n0, p.K - k0,
+                      p.vecB, tid, nthr);
     };
 
-    const FragBase<RT> fa = frag_base<RT>(ty, p.wgr);
-    const FragBase<CT> fb = frag_base<CT>(tx, p.wgc);
+    using FragA = Frag<!TA, RT, ACC>;
+    using FragB = Frag<TB, CT, ACC>;
+    FragA fa;
+    FragB fb;
+    fa.init(ty, p.wgr);
+    fb.init(tx, p.wgc);
     float acc[RT][CT];
 #pragma unroll
     for (int i = 0; i < RT; ++i)
@@ -265,11 +294,8 @@ __global__ void __launch_bounds__(256, 2) simt_gemm_kernel(const Params p) {
         for (int kb = 0; kb < BK; kb += ACC) {
             float a[ACC][RT];
             float b[ACC][CT];
-#pragma unroll
-            for (int kk = 0; kk < ACC; ++kk) {
-                load_frag<RT>(a_s, fa, kb + kk, a[kk]);
-                load_frag<CT>(b_s, fb, kb + kk, b[kk]);
-            }
+            fa.load(a_s, kb, a);
+            fb.load(b_s, kb, b);
 #pragma unroll
             for (int kk = 0; kk < ACC; ++kk)
 #pragma unroll
@@ -283,10 +309,10 @@ __global__ void __launch_bounds__(256, 2) simt_gemm_kernel(const Params p) {
     // epilogue: C = alpha*acc (+ beta*C)
 #pragma unroll
     for (int i = 0; i < RT; ++i) {
-        const int m = m0 + frag_index<RT>(i, ty, p.wgr);
+        const int m = m0 + FragA::index(i, ty, p.wgr);
         if (m >= p.M) continue;
         float* crow = C + (int64_t)m * p.ldc;
-        if constexpr (CT >= 4) {
+        if constexpr (!TB && CT >= 4) {
 #pragma unroll
             for (int q = 0; q < CT / 4; ++q) {
                 const int n = n0 + q * 4 * p.wgc + tx * 4;
@@ -313,7 +339,7 @@ __global__ void __launch_bounds__(256, 2) simt_gemm_kernel(const Params p) {
         } else {
 #pragma unroll
             for (int j = 0; j < CT; ++j) {
-                const int n = n0 + frag_index<CT>(j, tx, p.wgc);
+                const int n = n0 + FragB::index(j, tx, p.wgc);
                 if (n < p.N) crow[n] = epilogue(acc[i][j], p.alpha, p.beta, crow + n);
             }
         }
@@ -333,10 +359,10 @@ struct SmemPlan {
     size_t bytes;
 };
 
-inline SmemPlan plan_smem(int bm, int bn) {
+inline SmemPlan plan_smem(bool a_rows, bool b_rows, int bm, int bn) {
     SmemPlan s;
-    s.a_elems = (round4(bm) / 4) * CH;
-    s.b_elems = (round4(bn) / 4) * CH;
+    s.a_elems = a_rows ? bm * RS : (round4(bm) / 4) * CH;
+    s.b_elems = b_rows ? bn * RS : (round4(bn) / 4) * CH;
     const size_t stage = 4u * size_t(s.a_elems + s.b_elems);
     s.stages = (3 * stage <= 112 * 1024) ? 3 : 2;
     s.bytes = s.stages * stage;
@@ -346,7 +372,7 @@ inline SmemPlan plan_smem(int bm, int bn) {
 template <int ACC, int RT, int CT, bool TA, bool TB>
 kp_status launch(const GemmProblem& g, int wgr, int wgc, cudaStream_t stream) {
     const int bm = RT * wgr, bn = CT * wgc;
-    const SmemPlan sp = plan_smem(bm, bn);
+    const SmemPlan sp = plan_smem(!TA, TB, bm, bn);
     if (sp.bytes > 227 * 1024) return fail(KP_ERR_UNSUPPORTED, "simt: shared-memory plan too large");
     auto kern = simt_gemm_kernel<ACC, RT, CT, TA, TB>;
     static bool attr_done = false;  // idempotent; one process drives one device
@@ -367,9 +393,10 @@ kp_status launch(const GemmProblem& g, int wgr, int wgc, cudaStream_t stream) {
     p.log_bm = ilog2(bm); p.log_bn = ilog2(bn);
     p.stages = sp.stages;
     const bool multi = g.batch > 1;
-    // 16-byte copies need 16-byte aligned rows of the m/n-contiguous operands
-    p.vecA = TA && aligned16(g.A) && g.lda % 4 == 0 && (!multi || g.sa % 4 == 0) && bm % 4 == 0;
-    p.vecB = !TB && aligned16(g.B) && g.ldb % 4 == 0 && (!multi || g.sb % 4 == 0) && bn % 4 == 0;
+    // 16-byte copies need 16-byte aligned rows (and a 4-aligned tile extent for
+    // the chunk layout of m/n-contiguous operands)
+    p.vecA = aligned16(g.A) && g.lda % 4 == 0 && (!multi || g.sa % 4 == 0) && (!TA || bm % 4 == 0);
+    p.vecB = aligned16(g.B) && g.ldb % 4 == 0 && (!multi || g.sb % 4 == 0) && (TB || bn % 4 == 0);
     p.vecC = aligned16(g.C) && g.ldc % 4 == 0 && (!multi || g.sc % 4 == 0);
     p.tiles_m = int((g.m + bm - 1) / bm);
     p.tiles_n = int((g.n + bn - 1) / bn);
