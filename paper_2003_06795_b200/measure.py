@@ -80,8 +80,18 @@ def _operands(problem: ProblemSize, spec: SweepSpec, index: int, device):
     if bt > 1:
         a_shape, b_shape = (bt,) + a_shape, (bt,) + b_shape
     dtype = torch.bfloat16 if spec.family == "bf16" else torch.float32
-    a = (torch.rand(a_shape, generator=gen) * 2 - 1).to(device=device, dtype=dtype)
-    b = (torch.rand(b_shape, generator=gen) * 2 - 1).to(device=device, dtype=dtype)
+    # tensor-core families load through TMA, which needs 16-byte row pitches:
+    # the sweep pads the leading dimension of its own allocations (the
+    # logical shape is unchanged; TMA zero-fills past the logical extent)
+    align = {"tf32": 4, "bf16": 8}.get(spec.family, 1)
+
+    def alloc(shape):
+        inner = -(-shape[-1] // align) * align
+        full = (torch.rand(shape[:-1] + (inner,), generator=gen) * 2 - 1)
+        return full.to(device=device, dtype=dtype)[..., :shape[-1]]
+
+    a = alloc(a_shape)
+    b = alloc(b_shape)
     if spec.trans_a:
         a = a.transpose(-1, -2)
     if spec.trans_b:
