@@ -22,7 +22,10 @@
 //   acc      1,2,4,8  -> pipeline stages 2, 3, 4, 6 (clamped to shared memory)
 //   row_tile 1        -> BM = 128 (cta_group::1)
 //   wg       (8, 8)   -> one tile per CTA, grouped raster
-// 16 configs per family, canonical KernelConfig order.
+//   wg     (16, 16)   -> persistent CTAs (grid = SM count), double-buffered
+//                        TMEM accumulator: epilogue of tile i overlaps the
+//                        MMAs of tile i+1
+// 32 configs per family, canonical KernelConfig order.
 #include <cuda.h>
 
 #include <algorithm>
@@ -47,6 +50,7 @@ struct TcParams {
     float alpha, beta;
     int tiles_m, tiles_n;
     int stages, k_tiles;
+    int batch;
     int a_batch, b_batch;  // 1 if the operand advances with the batch index, else 0
 };
 
@@ -175,7 +179,27 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
 }
 
 // ------------------------------------------------------------------ kernel
-template <int ES, int BN, bool A_MN, bool B_MN>
+// Tile t (0 <= t < tiles_m*tiles_n*batch): batch-major, then a grouped raster
+// of GROUP_M m-tiles sweeping n inside each batch.
+__device__ __forceinline__ void tile_coords(int t, const TcParams& p, int bn, int& m0, int& n0,
+                                            int& bz) {
+    const int per_batch = p.tiles_m * p.tiles_n;
+    bz = t / per_batch;
+    const int tile = t - bz * per_batch;
+    const int per_group = GROUP_M * p.tiles_n;
+    const int group = tile / per_group;
+    const int first_m = group * GROUP_M;
+    const int gsz = min(p.tiles_m - first_m, GROUP_M);
+    const int in_group = tile - group * per_group;
+    m0 = (first_m + in_group % gsz) * BM;
+    n0 = (in_group / gsz) * bn;
+}
+
+// NBUF = 1: one tile per CTA (grid = tiles). NBUF = 2: persistent CTAs (grid
+// = SM count) striding over tiles with a double-buffered TMEM accumulator, so
+// the epilogue of tile i overlaps the MMAs of tile i+1 and the TMA ring runs
+// ahead across tile boundaries.
+template <int ES, int BN, bool A_MN, bool B_MN, int NBUF>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                const TcParams p) {
@@ -188,6 +212,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     constexpr uint32_t B_BYTES = BN * ROW;
     constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
     constexpr uint32_t IDESC = instr_desc<ES, A_MN, B_MN, BN>();
+    constexpr uint32_t TMEM_COLS = BN * NBUF;
 
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte aligned stage ring, then barriers, TMEM slot, epilogue staging
@@ -195,39 +220,35 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     const uint32_t base = (raw + STAGE_ALIGN - 1) & ~uint32_t(STAGE_ALIGN - 1);
     uint8_t* gbase = smem_raw + (base - raw);
     const int S = p.stages;
-    const uint32_t bars = base + S * STAGE_BYTES;              // full[S], empty[S], done
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + S * STAGE_BYTES + (2 * S + 1) * 8);
-    float* staging = reinterpret_cast<float*>(gbase + S * STAGE_BYTES + (2 * S + 2) * 8);
+    // barriers: full[S], empty[S], acc_full[2], acc_empty[2]
+    const uint32_t bars = base + S * STAGE_BYTES;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + S * STAGE_BYTES + (2 * S + 4) * 8);
+    float* staging = reinterpret_cast<float*>(gbase + S * STAGE_BYTES + (2 * S + 5) * 8);
     auto full_bar = [&](int s) { return bars + 8u * s; };
     auto empty_bar = [&](int s) { return bars + 8u * (S + s); };
-    const uint32_t done_bar = bars + 8u * (2 * S);
+    auto acc_full = [&](int b) { return bars + 8u * (2 * S + b); };
+    auto acc_empty = [&](int b) { return bars + 8u * (2 * S + 2 + b); };
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-
-    const int tile = blockIdx.x;
-    const int per_group = GROUP_M * p.tiles_n;
-    const int group = tile / per_group;
-    const int first_m = group * GROUP_M;
-    const int gsz = min(p.tiles_m - first_m, GROUP_M);
-    const int in_group = tile - group * per_group;
-    const int m0 = (first_m + in_group % gsz) * BM;
-    const int n0 = (in_group / gsz) * BN;
-    const int bz = blockIdx.z;
+    const int total = p.tiles_m * p.tiles_n * p.batch;
 
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(full_bar(s), 1);
             mbar_init(empty_bar(s), 1);
         }
-        mbar_init(done_bar, 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(acc_full(b), 1);
+            mbar_init(acc_empty(b), 4);  // one arrival per epilogue warp
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
         asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
-                     :: "r"(smem_u32(tmem_slot)), "r"(BN) : "memory");
+                     :: "r"(smem_u32(tmem_slot)), "r"(TMEM_COLS) : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
     fence_before_sync();
@@ -236,93 +257,122 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     const uint32_t tmem = *tmem_slot;
 
     if (warp == 0) {
-        if (lane == 0) {  // ---- TMA producer
-            const int za = bz * p.a_batch, zb = bz * p.b_batch;
-            for (int kt = 0; kt < p.k_tiles; ++kt) {
-                const int s = kt % S;
-                const uint32_t phase = (kt / S) & 1;
-                mbar_wait(empty_bar(s), phase ^ 1);
-                mbar_expect_tx(full_bar(s), STAGE_BYTES);
-                const uint32_t sa = base + s * STAGE_BYTES;
-                const uint32_t sb = sa + A_BYTES;
-                const int k0 = kt * BK;
-                if constexpr (!A_MN) {
-                    tma_load_3d(sa, &map_a, k0, m0, za, full_bar(s));
-                } else {
+        if (lane == 0) {  // ---- TMA producer: one ring across all of this CTA's tiles
+            int kt_all = 0;
+            for (int t = blockIdx.x; t < total; t += gridDim.x) {
+                int m0, n0, bz;
+                tile_coords(t, p, BN, m0, n0, bz);
+                const int za = bz * p.a_batch, zb = bz * p.b_batch;
+                for (int kt = 0; kt < p.k_tiles; ++kt, ++kt_all) {
+                    const int s = kt_all % S;
+                    const uint32_t phase = (kt_all / S) & 1;
+                    mbar_wait(empty_bar(s), phase ^ 1);
+                    mbar_expect_tx(full_bar(s), STAGE_BYTES);
+                    const uint32_t sa = base + s * STAGE_BYTES;
+                    const uint32_t sb = sa + A_BYTES;
+                    const int k0 = kt * BK;
+                    if constexpr (!A_MN) {
+                        tma_load_3d(sa, &map_a, k0, m0, za, full_bar(s));
+                    } else {
 #pragma unroll
-                    for (int j = 0; j < BM / MA::ATOM; ++j)
-                        tma_load_3d(sa + j * BK * MA::W, &map_a, m0 + j * MA::ATOM, k0, za, full_bar(s));
-                }
-                if constexpr (!B_MN) {
-                    tma_load_3d(sb, &map_b, k0, n0, zb, full_bar(s));
-                } else {
+                        for (int j = 0; j < BM / MA::ATOM; ++j)
+                            tma_load_3d(sa + j * BK * MA::W, &map_a, m0 + j * MA::ATOM, k0, za,
+                                        full_bar(s));
+                    }
+                    if constexpr (!B_MN) {
+                        tma_load_3d(sb, &map_b, k0, n0, zb, full_bar(s));
+                    } else {
 #pragma unroll
-                    for (int j = 0; j < BN / MB::ATOM; ++j)
-                        tma_load_3d(sb + j * BK * MB::W, &map_b, n0 + j * MB::ATOM, k0, zb, full_bar(s));
+                        for (int j = 0; j < BN / MB::ATOM; ++j)
+                            tma_load_3d(sb + j * BK * MB::W, &map_b, n0 + j * MB::ATOM, k0, zb,
+                                        full_bar(s));
+                    }
                 }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {  // ---- MMA issuer
-            for (int kt = 0; kt < p.k_tiles; ++kt) {
-                const int s = kt % S;
-                const uint32_t phase = (kt / S) & 1;
-                mbar_wait(full_bar(s), phase);
+            int kt_all = 0, it = 0;
+            for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+                const int buf = NBUF == 2 ? (it & 1) : 0;
+                const uint32_t use = NBUF == 2 ? ((it >> 1) & 1) : (it & 1);
+                mbar_wait(acc_empty(buf), use ^ 1);  // epilogue drained this buffer
                 fence_after_sync();
-                const uint32_t sa = base + s * STAGE_BYTES;
-                const uint32_t sb = sa + A_BYTES;
+                const uint32_t d = tmem + uint32_t(buf * BN);
+                for (int kt = 0; kt < p.k_tiles; ++kt, ++kt_all) {
+                    const int s = kt_all % S;
+                    const uint32_t phase = (kt_all / S) & 1;
+                    mbar_wait(full_bar(s), phase);
+                    fence_after_sync();
+                    const uint32_t sa = base + s * STAGE_BYTES;
+                    const uint32_t sb = sa + A_BYTES;
 #pragma unroll
-                for (int k = 0; k < BK / UMMA_K; ++k) {
-                    // K-major: advance 32 B inside the 128B-swizzled row (8-row
-                    // groups, SBO 1024); MN-major: advance UMMA_K rows of W bytes,
-                    // LBO = one atom column block (BK rows), SBO = one swizzle group
-                    const uint64_t da =
-                        A_MN ? smem_desc(sa + k * UMMA_K * MA::W, BK * MA::W, MA::SBO, MA::LAYOUT)
-                             : smem_desc(sa + k * 32, 16, 1024, 2);
-                    const uint64_t db =
-                        B_MN ? smem_desc(sb + k * UMMA_K * MB::W, BK * MB::W, MB::SBO, MB::LAYOUT)
-                             : smem_desc(sb + k * 32, 16, 1024, 2);
-                    mma<ES>(tmem, da, db, IDESC, (kt | k) != 0);
+                    for (int k = 0; k < BK / UMMA_K; ++k) {
+                        // K-major: advance 32 B inside the 128B-swizzled row (8-row
+                        // groups, SBO 1024); MN-major: advance UMMA_K rows of W bytes,
+                        // LBO = one atom column block (BK rows), SBO = one swizzle group
+                        const uint64_t da =
+                            A_MN ? smem_desc(sa + k * UMMA_K * MA::W, BK * MA::W, MA::SBO, MA::LAYOUT)
+                                 : smem_desc(sa + k * 32, 16, 1024, 2);
+                        const uint64_t db =
+                            B_MN ? smem_desc(sb + k * UMMA_K * MB::W, BK * MB::W, MB::SBO, MB::LAYOUT)
+                                 : smem_desc(sb + k * 32, 16, 1024, 2);
+                        mma<ES>(d, da, db, IDESC, (kt | k) != 0);
+                    }
+                    umma_commit(empty_bar(s));  // frees the stage once these MMAs retire
                 }
-                umma_commit(empty_bar(s));  // frees the stage once these MMAs retire
+                umma_commit(acc_full(buf));     // accumulator of this tile complete
             }
-            umma_commit(done_bar);          // accumulator complete
         }
     } else {  // ---- epilogue warps 2..5: TMEM lane quarter = warp % 4
         const int q = warp & 3;
         float* st = staging + (warp - 2) * 32 * EPI_PITCH;
-        mbar_wait(done_bar, 0);
-        fence_after_sync();
-        float* Cb = p.C + int64_t(bz) * p.sc;
-        const int row0 = m0 + q * 32;
+        int it = 0;
+        for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+            int m0, n0, bz;
+            tile_coords(t, p, BN, m0, n0, bz);
+            const int buf = NBUF == 2 ? (it & 1) : 0;
+            const uint32_t use = NBUF == 2 ? ((it >> 1) & 1) : (it & 1);
+            mbar_wait(acc_full(buf), use);
+            fence_after_sync();
+            float* Cb = p.C + int64_t(bz) * p.sc;
+            const int row0 = m0 + q * 32;
+            const uint32_t taddr = tmem + (uint32_t(q * 32) << 16) + uint32_t(buf * BN);
+            const int cols = min(BN, p.N - n0);
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 32) {
-            float v[32];
-            tmem_ld32(tmem + (uint32_t(q * 32) << 16) + c0, v);
+            for (int c0 = 0; c0 < cols; c0 += 32) {
+                float v[32];
+                tmem_ld32(taddr + c0, v);
 #pragma unroll
-            for (int j = 0; j < 32; ++j) st[lane * EPI_PITCH + j] = v[j];
-            __syncwarp();
-            const int n = n0 + c0 + lane;
-            if (n < p.N) {
+                for (int j = 0; j < 32; ++j) st[lane * EPI_PITCH + j] = v[j];
+                __syncwarp();
+                const int n = n0 + c0 + lane;
+                if (n < p.N) {
 #pragma unroll 4
-                for (int r = 0; r < 32; ++r) {
-                    const int m = row0 + r;
-                    if (m < p.M) {
-                        float* dst = Cb + int64_t(m) * p.ldc + n;
-                        const float x = p.alpha * st[r * EPI_PITCH + lane];
-                        *dst = p.beta == 0.0f ? x : fmaf(p.beta, *dst, x);
+                    for (int r = 0; r < 32; ++r) {
+                        const int m = row0 + r;
+                        if (m < p.M) {
+                            float* dst = Cb + int64_t(m) * p.ldc + n;
+                            const float x = p.alpha * st[r * EPI_PITCH + lane];
+                            *dst = p.beta == 0.0f ? x : fmaf(p.beta, *dst, x);
+                        }
                     }
                 }
+                __syncwarp();
             }
-            __syncwarp();
+            fence_before_sync();
+            if (lane == 0) {
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(acc_empty(buf))
+                             : "memory");
+            }
         }
     }
     fence_before_sync();
     __syncthreads();
     if (warp == 1) {
         fence_after_sync();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(BN)
-                     : "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem),
+                     "r"(TMEM_COLS) : "memory");
     }
 }
 
@@ -371,28 +421,44 @@ static int tidx(uint32_t v) {
     return -1;
 }
 
-int32_t num_configs(kp_family fam) { return (fam == KP_TF32_TC || fam == KP_BF16_TC) ? 16 : 0; }
+// Config list per family: acc x col_tile x {wg (8,8): one tile per CTA,
+// wg (16,16): persistent CTAs with a double-buffered TMEM accumulator}.
+int32_t num_configs(kp_family fam) { return (fam == KP_TF32_TC || fam == KP_BF16_TC) ? 32 : 0; }
 
 kp_status config_at(kp_family fam, int32_t index, kp_config* out) {
     if (index < 0 || index >= num_configs(fam)) return fail(KP_ERR_INVALID_ARG, "config index out of range");
-    *out = kp_config{kTiles[index / 4], 1u, kTiles[index % 4], 8u, 8u};
+    const uint32_t wg = (index % 2) ? 16u : 8u;
+    *out = kp_config{kTiles[index / 8], 1u, kTiles[(index / 2) % 4], wg, wg};
     return KP_OK;
 }
 
 kp_status valid(kp_family fam, const kp_config& c) {
     if (num_configs(fam) == 0) return fail(KP_ERR_INVALID_ARG, "not a tensor-core family");
-    if (tidx(c.acc) < 0 || c.row_tile != 1 || tidx(c.col_tile) < 0 || c.wg_rows != 8 || c.wg_cols != 8)
+    const bool wg_ok = (c.wg_rows == 8 && c.wg_cols == 8) || (c.wg_rows == 16 && c.wg_cols == 16);
+    if (tidx(c.acc) < 0 || c.row_tile != 1 || tidx(c.col_tile) < 0 || !wg_ok)
         return fail(KP_ERR_INVALID_CONFIG,
-                    "tcgen05 family configs are (acc in 1,2,4,8; row_tile 1; col_tile in 1,2,4,8; wg 8x8)");
+                    "tcgen05 family configs are (acc in 1,2,4,8; row_tile 1; col_tile in 1,2,4,8; "
+                    "wg 8x8 or 16x16)");
     return KP_OK;
 }
 
 static size_t smem_bytes(int bn, int stages) {
-    return STAGE_ALIGN + size_t(stages) * (BM + bn) * 128 + (2 * stages + 2) * 8 +
+    return STAGE_ALIGN + size_t(stages) * (BM + bn) * 128 + (2 * stages + 6) * 8 +
            4 * 32 * EPI_PITCH * 4;
 }
 
-template <int ES, int BN, bool A_MN, bool B_MN>
+static int sm_count() {
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+template <int ES, int BN, bool A_MN, bool B_MN, int NBUF>
 static kp_status launch_t(const GemmProblem& g, int want_stages, cudaStream_t stream) {
     int stages = want_stages;
     while (stages > 2 && smem_bytes(BN, stages) > 227 * 1024) --stages;
@@ -411,7 +477,7 @@ static kp_status launch_t(const GemmProblem& g, int want_stages, cudaStream_t st
     if (!B_MN) st = make_map(&mb, bf16, g.B, g.k, g.n, bat_b, g.ldb, g.sb, BK, BN, sw128);
     else       st = make_map(&mb, bf16, g.B, g.n, g.k, bat_b, g.ldb, g.sb, MB::ATOM, BK, MB::TMA_SWIZZLE);
     if (st != KP_OK) return st;
-    auto kern = tc_gemm_kernel<ES, BN, A_MN, B_MN>;
+    auto kern = tc_gemm_kernel<ES, BN, A_MN, B_MN, NBUF>;
     static bool attr_done = false;
     if (!attr_done) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
@@ -427,33 +493,35 @@ static kp_status launch_t(const GemmProblem& g, int want_stages, cudaStream_t st
     p.tiles_n = int((g.n + BN - 1) / BN);
     p.stages = stages;
     p.k_tiles = int((g.k + BK - 1) / BK);
+    p.batch = int(g.batch);
     p.a_batch = g.sa ? 1 : 0;
     p.b_batch = g.sb ? 1 : 0;
-    const int64_t tiles = int64_t(p.tiles_m) * p.tiles_n;
-    if (tiles > 0x7fffffffLL || g.batch > 65535) return fail(KP_ERR_BAD_SHAPE, "tc: grid too large");
-    kern<<<dim3(unsigned(tiles), 1, unsigned(g.batch)), NUM_THREADS, smem, stream>>>(ma, mb, p);
+    const int64_t tiles = int64_t(p.tiles_m) * p.tiles_n * g.batch;
+    if (tiles > 0x7fffffffLL) return fail(KP_ERR_BAD_SHAPE, "tc: grid too large");
+    const int64_t grid = NBUF == 2 ? std::min<int64_t>(tiles, sm_count()) : tiles;
+    kern<<<dim3(unsigned(grid)), NUM_THREADS, smem, stream>>>(ma, mb, p);
     note_launch();
     return check_launch("tc_gemm_kernel");
 }
 
-template <int ES, int BN>
+template <int ES, int BN, int NBUF>
 static kp_status by_layout(const GemmProblem& g, int stages, cudaStream_t s) {
     // A normal = K-major, A transposed = MN-major; B transposed = K-major, B normal = MN-major
-    if (!g.ta && g.tb) return launch_t<ES, BN, false, false>(g, stages, s);
-    if (!g.ta && !g.tb) return launch_t<ES, BN, false, true>(g, stages, s);
-    if (g.ta && g.tb) return launch_t<ES, BN, true, false>(g, stages, s);
-    return launch_t<ES, BN, true, true>(g, stages, s);
+    if (!g.ta && g.tb) return launch_t<ES, BN, false, false, NBUF>(g, stages, s);
+    if (!g.ta && !g.tb) return launch_t<ES, BN, false, true, NBUF>(g, stages, s);
+    if (g.ta && g.tb) return launch_t<ES, BN, true, false, NBUF>(g, stages, s);
+    return launch_t<ES, BN, true, true, NBUF>(g, stages, s);
 }
 
-template <int ES>
+template <int ES, int NBUF>
 static kp_status by_tile(const kp_config& c, const GemmProblem& g, cudaStream_t s) {
     static const int kStages[4] = {2, 3, 4, 6};
     const int stages = kStages[tidx(c.acc)];
     switch (c.col_tile) {
-        case 1: return by_layout<ES, 32>(g, stages, s);
-        case 2: return by_layout<ES, 64>(g, stages, s);
-        case 4: return by_layout<ES, 128>(g, stages, s);
-        case 8: return by_layout<ES, 256>(g, stages, s);
+        case 1: return by_layout<ES, 32, NBUF>(g, stages, s);
+        case 2: return by_layout<ES, 64, NBUF>(g, stages, s);
+        case 4: return by_layout<ES, 128, NBUF>(g, stages, s);
+        case 8: return by_layout<ES, 256, NBUF>(g, stages, s);
     }
     return fail(KP_ERR_INVALID_CONFIG, "tc: bad col_tile");
 }
@@ -468,7 +536,9 @@ kp_status launch(kp_family fam, const kp_config& c, const GemmProblem& g, cudaSt
     if (!al(g.A, g.lda, g.sa) || !al(g.B, g.ldb, g.sb))
         return fail(KP_ERR_ALIGNMENT,
                     "tcgen05 families need 16-byte aligned operands and row/batch pitches");
-    return fam == KP_BF16_TC ? by_tile<2>(c, g, s) : by_tile<4>(c, g, s);
+    const bool persistent = c.wg_rows == 16;
+    if (fam == KP_BF16_TC) return persistent ? by_tile<2, 2>(c, g, s) : by_tile<2, 1>(c, g, s);
+    return persistent ? by_tile<4, 2>(c, g, s) : by_tile<4, 1>(c, g, s);
 }
 
 }  // namespace tc

@@ -49,7 +49,7 @@ def _check(family, cfg, m, k, n, ta, tb, batch=1, seed=0):
 @pytest.mark.parametrize("family", ["bf16", "tf32"])
 def test_family_configs_enumerate(family):
     cfgs = _gemm().family_configs(family)
-    assert len(cfgs) == 16
+    assert len(cfgs) == 32
     assert list(cfgs) == sorted(cfgs)
 
 
