@@ -200,13 +200,137 @@ def traffic_for(cfg, size):
     return None if ent is None else ent.get("dram_bytes")
 
 
+def tensor_peak(family: str):
+    """(peak TFLOP/s, source) for a tcgen05 family: MEASURED_PEAKS.json's bf16
+    burst figure (TF32 dense = half of it, NVIDIA's dense ratio), else the
+    B200_PROFILING.md fallback."""
+    path = ROOT / "MEASURED_PEAKS.json"
+    if path.exists():
+        bf16 = float(json.loads(path.read_text())["bf16_tflops"])
+        src = "MEASURED_PEAKS.json bf16_tflops (burst)"
+    else:
+        bf16, src = 1590.0, "fallback 1.59 PFLOP/s (B200_PROFILING.md)"
+    if family == "tf32":
+        return bf16 / 2, src + " / 2 (tf32 dense rate)"
+    return bf16, src
+
+
+class FamilyRun:
+    """Sweep + timed selected-kernel steps of one kernel family on the square
+    set (one rank's share; gathered / max-reduced by the caller)."""
+
+    def __init__(self, family, args, dev, rank, world, gloo):
+        import torch
+        from paper_2003_06795_b200 import gemm, measure
+        self.family, self.args, self.dev = family, args, dev
+        self.rank, self.world, self.gloo = rank, world, gloo
+        self.gemm, self.measure, self.torch = gemm, measure, torch
+        dt = torch.bfloat16 if family == "bf16" else torch.float32
+        gen = torch.Generator(device="cpu").manual_seed(1234 + rank)
+        self.probs = []
+        for s in SIZES:
+            a = (torch.rand((s, s), generator=gen) * 2 - 1).to(dev).to(dt)
+            b = (torch.rand((s, s), generator=gen) * 2 - 1).to(dev).to(dt)
+            self.probs.append((s, a, b, torch.empty((s, s), device=dev)))
+        # raises if no selector is compiled in for this family (no fallback)
+        self.selected = [gemm.select(s, s, s, family=family) for s in SIZES]
+        self.configs = gemm.family_configs(family)
+
+    def barrier(self):
+        import torch.distributed as dist
+        if self.world > 1:
+            dist.barrier()
+        self.torch.cuda.synchronize()
+
+    def sweep(self):
+        import torch.distributed as dist
+        mine = self.measure.config_shard(len(self.configs), self.rank, self.world)
+        cells = {}
+        self.barrier()
+        t0 = time.perf_counter()
+        if not self.args.no_sweep:
+            for i, (s, a, b, c) in enumerate(self.probs):
+                res = self.gemm.sweep_problem(a, b, [self.configs[j] for j in mine], out=c,
+                                              family=self.family, warmup=1,
+                                              reps=self.args.sweep_reps, min_sample_ns=20_000.0,
+                                              max_cell_ns=5e6)
+                cells.update({(i, j): ns for j, ns in zip(mine, res)})
+        self.barrier()
+        wall = time.perf_counter() - t0
+        if self.world > 1:
+            walls = [None] * self.world
+            dist.all_gather_object(walls, wall, group=self.gloo)
+            wall = max(walls)
+        self.cells = self.measure.gather_cells(cells, self.world, self.gloo)
+        self.sweep_wall = wall
+
+    def timed(self, steps, clocks=None):
+        """Per-size kernel ms over `steps` timed steps (L2 flushed before each
+        kernel, CUDA events on the launching stream)."""
+        import numpy as np
+        torch = self.torch
+        flush = torch.empty(FLUSH_BYTES // 4, device=self.dev)
+        stream = torch.cuda.current_stream()
+        n = self.args.warmup + steps
+        ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in SIZES] for _ in range(n)]
+        launches0 = 0
+        for step in range(n):
+            if step == self.args.warmup:
+                self.barrier()
+                if clocks:
+                    clocks.start()
+                launches0 = self.gemm.launch_count()
+            for i, (s, a, b, c) in enumerate(self.probs):
+                flush.zero_()
+                ev[step][i][0].record(stream)
+                self.gemm.matmul(a, b, None, out=c, family=self.family)
+                ev[step][i][1].record(stream)
+        self.barrier()
+        launches = self.gemm.launch_count() - launches0
+        ms = np.array([[ev[st][i][0].elapsed_time(ev[st][i][1]) for i in range(len(SIZES))]
+                       for st in range(self.args.warmup, n)])
+        return ms, launches
+
+    def report(self, per_size_ms):
+        import numpy as np
+        mean_ms = per_size_ms.mean(axis=0)
+        per_size, ratios = [], []
+        for i, s in enumerate(SIZES):
+            entry = {"size": s, "config": list(self.selected[i].as_tuple()),
+                     "tflops": flops_of(s) / (mean_ms[i] * 1e-3) / 1e12}
+            if self.cells:
+                row = np.array([self.cells[(i, j)] for j in range(len(self.configs))])
+                jbest, jsel = int(row.argmin()), self.configs.index(self.selected[i])
+                ratios.append(row[jbest] / row[jsel])
+                entry.update(best_config=list(self.configs[jbest].as_tuple()),
+                             best_tflops_warm=flops_of(s) / row[jbest] / 1e3,
+                             selected_tflops_warm=flops_of(s) / row[jsel] / 1e3)
+            per_size.append(entry)
+        pct = (100.0 * math.exp(sum(math.log(r) for r in ratios) / len(ratios))
+               if ratios else None)
+        dom = int(mean_ms.argmax())
+        return per_size, pct, dom, mean_ms
+
+
+def max_over_ranks(x, world, dev):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def run_gpu(args) -> int:
-    import numpy as np
+    import ctypes
+
     import torch
     import torch.distributed as dist
 
-    from paper_2003_06795_b200 import gemm, measure
-    from paper_2003_06795_b200.dataset import all_configs
+    from paper_2003_06795_b200 import _native as nat
+    from paper_2003_06795_b200 import gemm
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -217,133 +341,69 @@ def run_gpu(args) -> int:
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
         gloo = dist.new_group(backend="gloo")
+    step_flops = sum(flops_of(s) for s in SIZES)
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-
-    gen = torch.Generator(device="cpu").manual_seed(1234 + rank)
-    probs = []
-    for s in SIZES:
-        a = (torch.rand((s, s), generator=gen) * 2 - 1).to(dev)
-        b = (torch.rand((s, s), generator=gen) * 2 - 1).to(dev)
-        c = torch.empty((s, s), device=dev)
-        probs.append((s, a, b, c))
-    selected = [gemm.select(s, s, s) for s in SIZES]  # raises if no selector compiled in
-
-    # ---- 1. sweep (interleaved config shard per rank) -----------------------
-    configs = all_configs()
-    mine = measure.config_shard(len(configs), rank, world)
-    sweep = {}
-    barrier()
-    t0 = time.perf_counter()
-    if not args.no_sweep:
-        for i, (s, a, b, c) in enumerate(probs):
-            res = gemm.sweep_problem(a, b, [configs[j] for j in mine], out=c, warmup=1,
-                                     reps=args.sweep_reps, min_sample_ns=20_000.0,
-                                     max_cell_ns=5e6)
-            for j, ns in zip(mine, res):
-                sweep[(i, j)] = ns
-    barrier()
-    sweep_wall = time.perf_counter() - t0
-    if world > 1:
-        walls = [None] * world
-        dist.all_gather_object(walls, sweep_wall, group=gloo)
-        sweep_wall = max(walls)
-    sweep = measure.gather_cells(sweep, world, gloo)
-
-    # ---- peaks for the roofline -------------------------------------------
-    import ctypes
-
-    from paper_2003_06795_b200 import _native as nat
+    # ---- headline family: FP32 SIMT (the paper's 640-config space) ---------
+    f32 = FamilyRun("f32", args, dev, rank, world, gloo)
+    f32.sweep()
     peak = ctypes.c_double()
     nat.check(nat.lib().kp_fp32_peak(ctypes.byref(peak), None), "kp_fp32_peak")
-
-    # ---- 2. timed steps: selected kernels, L2 flushed before each ---------
-    flush = torch.empty(FLUSH_BYTES // 4, device=dev)
-    stream = torch.cuda.current_stream()
-    n_steps = args.warmup + args.steps
-    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in SIZES] for _ in range(n_steps)]
     clocks = ClockSampler()
-    launches0 = None
-    for step in range(n_steps):
-        if step == args.warmup:
-            barrier()
-            clocks.start()
-            launches0 = gemm.launch_count()
-        for i, (s, a, b, c) in enumerate(probs):
-            flush.zero_()
-            ev[step][i][0].record(stream)
-            gemm.matmul(a, b, None, out=c)
-            ev[step][i][1].record(stream)
-    barrier()
-    launches = gemm.launch_count() - launches0
+    per_size_ms, launches = f32.timed(args.steps, clocks)
     clk = clocks.stop(gpu_index())
-    per_size_ms = np.array([[ev[st][i][0].elapsed_time(ev[st][i][1]) for i in range(len(SIZES))]
-                            for st in range(args.warmup, n_steps)])
-    total_ms = float(per_size_ms.sum())
+    total_ms = max_over_ranks(float(per_size_ms.sum()), world, dev)
     if world > 1:
-        t = torch.tensor([total_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
         lt = torch.tensor([launches], device=dev, dtype=torch.int64)
         dist.all_reduce(lt)
         launches = int(lt.item())
-    step_flops = sum(flops_of(s) for s in SIZES)
     value = world * args.steps * step_flops / (total_ms * 1e-3) / 1e12
 
-    # ---- 3. e2e through the host-buffer API --------------------------------
-    host = []
-    for s, a, b, c in probs:
-        host.append((a.cpu().pin_memory(), b.cpu().pin_memory(),
-                     torch.empty((s, s), pin_memory=True)))
+    # ---- e2e through the host-buffer API --------------------------------
+    host = [(a.cpu().pin_memory(), b.cpu().pin_memory(), torch.empty((s, s), pin_memory=True))
+            for s, a, b, c in f32.probs]
     for _ in range(args.warmup):
         for ha, hb, hc in host:
             gemm.matmul_pinned(ha, hb, hc)
-    barrier()
+    f32.barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
         for ha, hb, hc in host:
             gemm.matmul_pinned(ha, hb, hc)
-    e2e_s = time.perf_counter() - t0
-    if world > 1:
-        t = torch.tensor([e2e_s], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+    e2e_s = max_over_ranks(time.perf_counter() - t0, world, dev)
     e2e_value = world * args.steps * step_flops / e2e_s / 1e12
-    h2d = sum(2 * 4 * s * s for s in SIZES)
-    d2h = sum(4 * s * s for s in SIZES)
+
+    # ---- tensor-core families (same workload, their own selectors) -------
+    families = {}
+    fam_steps = max(20, args.steps // 4)
+    for fam in ("tf32", "bf16"):
+        run = FamilyRun(fam, args, dev, rank, world, gloo)
+        run.sweep()
+        ms, _ = run.timed(fam_steps)
+        tot = max_over_ranks(float(ms.sum()), world, dev)
+        per, pct, dom, mean = run.report(ms)
+        tpk, src = tensor_peak(fam)
+        ach = flops_of(SIZES[dom]) / (mean[dom] * 1e-3) / 1e12
+        families[fam] = {
+            "value": world * fam_steps * step_flops / (tot * 1e-3) / 1e12, "unit": "TFLOP/s",
+            "steps": fam_steps, "pct_oracle_best": pct,
+            "sweep": {"cells": len(run.cells), "cells_per_s":
+                      len(run.cells) / run.sweep_wall if run.cells else None},
+            "roofline": {"bound": "tensor", "achieved": ach, "peak": tpk, "unit": "TFLOP/s",
+                         "frac": ach / tpk, "peak_source": src,
+                         "kernel": f"tc_gemm {per[dom]['config']} @ {SIZES[dom]}^3"},
+            "per_size": per, "selector": f"csrc/generated/select_{fam}_nn.h"}
 
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return 0
 
-    # ---- per-size report, % of oracle-best ---------------------------------
-    mean_ms = per_size_ms.mean(axis=0)
-    per_size, ratios = [], []
-    for i, s in enumerate(SIZES):
-        entry = {"size": s, "config": list(selected[i].as_tuple()),
-                 "tflops": flops_of(s) / (mean_ms[i] * 1e-3) / 1e12}
-        if sweep:
-            row = np.array([sweep[(i, j)] for j in range(len(configs))])
-            jbest = int(row.argmin())
-            jsel = configs.index(selected[i])
-            ratios.append(row[jbest] / row[jsel])
-            entry.update(best_config=list(configs[jbest].as_tuple()),
-                         best_tflops_warm=flops_of(s) / row[jbest] / 1e3,
-                         selected_tflops_warm=flops_of(s) / row[jsel] / 1e3)
-        per_size.append(entry)
-    pct_best = (100.0 * math.exp(sum(math.log(r) for r in ratios) / len(ratios))
-                if ratios else None)
-    dom = int(mean_ms.argmax())  # kernel with the largest share of the step
+    per_size, pct_best, dom, mean_ms = f32.report(per_size_ms)
     achieved = flops_of(SIZES[dom]) / (mean_ms[dom] * 1e-3) / 1e12
     roofline = {"bound": "fp32-ffma", "achieved": achieved, "peak": peak.value,
                 "unit": "TFLOP/s", "frac": achieved / peak.value,
-                "traffic": traffic_for(selected[dom], SIZES[dom]),
-                "kernel": f"simt_gemm {list(selected[dom].as_tuple())} @ {SIZES[dom]}^3",
+                "traffic": traffic_for(f32.selected[dom], SIZES[dom]),
+                "kernel": f"simt_gemm {list(f32.selected[dom].as_tuple())} @ {SIZES[dom]}^3",
                 "share_of_step": float(mean_ms[dom] / mean_ms.sum()),
                 "peak_source": "measured FFMA microbenchmark (kp_fp32_peak) on this GPU; "
                                "MEASURED_PEAKS.json has no fp32 SIMT figure"}
@@ -358,16 +418,18 @@ def run_gpu(args) -> int:
                    "l2": f"flushed before every timed kernel ({FLUSH_BYTES >> 20} MiB write)",
                    "parallelism": f"replicas x{world}"},
         "pct_oracle_best": pct_best,
-        "sweep": {"cells": len(sweep), "wall_s": sweep_wall,
-                  "cells_per_s": len(sweep) / sweep_wall if sweep else None,
+        "sweep": {"cells": len(f32.cells), "wall_s": f32.sweep_wall,
+                  "cells_per_s": len(f32.cells) / f32.sweep_wall if f32.cells else None,
                   "timing": "warm L2, median of reps, C++ loop (kp_sweep_problem)"},
         "per_size": per_size,
         "roofline": roofline,
-        "e2e": {"value": e2e_value, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h,
+        "e2e": {"value": e2e_value, "unit": "TFLOP/s",
+                "h2d_bytes_per_step": sum(2 * 4 * s * s for s in SIZES),
+                "d2h_bytes_per_step": sum(4 * s * s for s in SIZES),
                 "path": "gemm.matmul_pinned: pinned H2D + kp_gemm_auto + D2H + sync"},
         "gpu_launches": launches,
         "clocks": clk,
+        "families": families,
     }
     if world == 1:
         line["cpu_baseline"] = cpu_baseline(args.cpu_seconds)

@@ -91,12 +91,20 @@ static kp_status to_problem(const kp_gemm_desc* d, const void* A, const void* B,
     return KP_OK;
 }
 
+#ifdef KP_LEAN
+// Lean library (the paper's deployment build): only the kernels named by the
+// compiled selectors exist; generated/simt_lean.cu provides the dispatch.
+namespace simt {
+kp_status lean_dispatch(const kp_config& c, int layout, const GemmProblem& g, cudaStream_t s);
+}
+#else
 static const simt::LaunchFn kSimt[16] = {
     simt::KP_SIMT_FN(1, 1), simt::KP_SIMT_FN(1, 2), simt::KP_SIMT_FN(1, 4), simt::KP_SIMT_FN(1, 8),
     simt::KP_SIMT_FN(2, 1), simt::KP_SIMT_FN(2, 2), simt::KP_SIMT_FN(2, 4), simt::KP_SIMT_FN(2, 8),
     simt::KP_SIMT_FN(4, 1), simt::KP_SIMT_FN(4, 2), simt::KP_SIMT_FN(4, 4), simt::KP_SIMT_FN(4, 8),
     simt::KP_SIMT_FN(8, 1), simt::KP_SIMT_FN(8, 2), simt::KP_SIMT_FN(8, 4), simt::KP_SIMT_FN(8, 8),
 };
+#endif
 
 static kp_status valid_config(kp_family fam, const kp_config& c) {
     if (fam == KP_F32_SIMT) {
@@ -115,8 +123,12 @@ static kp_status valid_config(kp_family fam, const kp_config& c) {
 static kp_status run(kp_family fam, const kp_config& c, const GemmProblem& g, cudaStream_t s) {
     if (fam == KP_F32_SIMT) {
         const int layout = (g.ta ? 2 : 0) + (g.tb ? 1 : 0);
+#ifdef KP_LEAN
+        return simt::lean_dispatch(c, layout, g, s);
+#else
         return kSimt[tile_index(c.acc) * 4 + tile_index(c.row_tile)](int(c.col_tile), layout, g,
                                                                       int(c.wg_rows), int(c.wg_cols), s);
+#endif
     }
     return tc::launch(fam, c, g, s);
 }

@@ -90,6 +90,11 @@ PROBLEM_SETS = {
     "networks": lambda: network_problems(batches=(1, 2, 4, 8, 16)),
     "networks-all": lambda: network_problems(),
     "networks-small": lambda: network_problems(batches=(1, 4), max_flops=2e9),
+    # selector training set: the network shapes plus the bench's square sizes
+    # (and 4096) so the deployed tree also covers BASELINE configs[1]
+    "networks+squares": lambda: tuple(dict.fromkeys(
+        network_problems(batches=(1, 2, 4, 8, 16))
+        + square_problems((64, 128, 256, 512, 1024, 2048, 4096)))),
 }
 
 

@@ -99,3 +99,28 @@ def test_status_strings():
     lib = nat.lib()
     for st in range(7):
         assert lib.kp_status_string(st)
+
+
+LEAN = Path(__file__).resolve().parents[1] / "paper_2003_06795_b200" / "libkp_lean.so"
+
+
+@pytest.mark.skipif(not LEAN.exists(), reason="lean library not built (build --lean)")
+def test_lean_library_only_has_selected_kernels():
+    """The paper's deployment build: only selector-reachable FP32 kernels are
+    compiled; any other config is rejected before a launch."""
+    import json
+    lib = ctypes.CDLL(str(LEAN))
+    nat._declare(lib)
+    for name in declared_symbols():
+        assert hasattr(lib, name), name
+    sel = json.loads((Path(__file__).resolve().parents[1] / "selectors" / "f32_nn" /
+                      "selection.json").read_text())
+    chosen = {(c["acc"], c["row_tile"], c["col_tile"]) for c in sel["configs"]}
+    missing = next(c for c in dataset.all_configs() if c.as_tuple()[:3] not in chosen)
+    d = _desc(m=8, k=8, n=8, lda=8, ldb=8, ldc=8, stride_c=64)
+    buf = ctypes.c_void_p(16)
+    rc = lib.kp_gemm(nat.F32_SIMT, nat.KpConfig(*missing.as_tuple()), ctypes.byref(d), buf, buf,
+                     buf, None)
+    assert rc == nat.KP_ERR_UNSUPPORTED
+    assert b"lean" in lib.kp_last_error()
+    assert LEAN.stat().st_size < nat.LIB_PATH.stat().st_size
