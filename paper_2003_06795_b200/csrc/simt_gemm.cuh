@@ -15,7 +15,7 @@
 //
 // B200 mapping:
 //   * shared memory keeps each operand in its global orientation, K depth
-//     BK = 16 per stage, 2/3-stage cp.async ring (16-byte copies when rows
+//     BK = 32 (16 for the largest tiles) per stage, 2/3-stage cp.async ring (16-byte copies when rows
 //     are 16-byte aligned, zero-filling 4-byte copies otherwise):
 //       m/n-contiguous sources (A transposed, B normal): "chunk" layout, 4
 //         output rows x BK K-slices per padded chunk (chunk_off); a thread
@@ -37,9 +37,17 @@
 namespace kp {
 namespace simt {
 
-constexpr int BK = 16;      // shared-memory K depth per pipeline stage
-constexpr int LOG_BK = 4;
 constexpr int GROUP_M = 8;  // tile raster: 8 m-tiles share a sweep over n
+
+// Shared K depth per pipeline stage: 32 when two stages of it fit in 112 KB
+// (two CTAs per SM), else 16 -- halves the per-K-slice copy/sync overhead of
+// the common tiles without starving the huge (1024-row) ones.
+template <int BK>
+struct Geo {
+    static constexpr int LOG_BK = BK == 32 ? 5 : 4;
+    static constexpr int CH = BK * 4 + 4;  // chunk pitch (floats), see chunk_off
+    static constexpr int RS = BK + 4;      // row pitch (floats), see copy_rows
+};
 
 struct Params {
     const float* A;
@@ -60,19 +68,22 @@ struct Params {
 // rows of the output axis is stored as BM/4 chunks of 4 consecutive rows, each
 // chunk holding its BK K-slices as 16-byte float4s:
 //     element (k, m)  at  (m >> 2) * CH + k * 4 + (m & 3),   CH = BK*4 + 4.
+// (CH/4 is odd, so 8 consecutive chunks start in 8 distinct bank groups.)
 // A thread's 4-row fragment at slice k is one LDS.128 whose offset is a
 // per-thread base plus the compile-time k*4, so the unrolled K loop needs no
 // address arithmetic (the runtime work-group shape only enters the bases);
 // the 4-float pad per chunk makes 8 consecutive chunks hit 8 different 16-byte
 // bank groups.
-constexpr int CH = BK * 4 + 4;
-
-__device__ __forceinline__ int chunk_off(int k, int m) { return (m >> 2) * CH + k * 4 + (m & 3); }
+template <int BK>
+__device__ __forceinline__ int chunk_off(int k, int m) {
+    return (m >> 2) * Geo<BK>::CH + k * 4 + (m & 3);
+}
 
 // Copy a BK x cols block whose rows are K and whose columns (the M/N axis,
 // cols = 1 << log_cols) are contiguous in global memory (element (k, c) at
 // src[k*ld + c]) into the chunk-major tile at shared address `s`. Elements
 // with k >= kv or c >= cv are written as zero. 16-byte copies when vec.
+template <int BK>
 __device__ __forceinline__ void copy_direct(uint32_t s, const float* src, int64_t ld, int log_cols,
                                             int cv, int kv, bool vec, int tid, int nthr) {
     if (vec && log_cols >= 2) {
@@ -87,7 +98,7 @@ __device__ __forceinline__ void copy_direct(uint32_t s, const float* src, int64_
             const int cbytes = min(max(cv - c0, 0), 4) * 4;
             const float* gp = src + (int64_t)r0 * ld + c0;
             const int64_t gstep = (int64_t)dr * ld;
-            const uint32_t sp = s + 4u * chunk_off(r0, c0);
+            const uint32_t sp = s + 4u * chunk_off<BK>(r0, c0);
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
                 if (c < n) {
@@ -100,7 +111,7 @@ __device__ __forceinline__ void copy_direct(uint32_t s, const float* src, int64_
         for (int idx = tid; idx < total; idx += nthr) {
             const int r = idx >> log_cpr;
             const int c = (idx & ((1 << log_cpr) - 1)) << 2;
-            cp_async16(s + 4u * chunk_off(r, c), src + (int64_t)r * ld + c,
+            cp_async16(s + 4u * chunk_off<BK>(r, c), src + (int64_t)r * ld + c,
                        r < kv ? min(max(cv - c, 0), 4) * 4 : 0);
         }
         return;
@@ -109,7 +120,7 @@ __device__ __forceinline__ void copy_direct(uint32_t s, const float* src, int64_
     for (int idx = tid; idx < total; idx += nthr) {
         const int r = idx >> log_cols;
         const int c = idx & ((1 << log_cols) - 1);
-        cp_async4(s + 4u * chunk_off(r, c), src + (int64_t)r * ld + c, (r < kv && c < cv) ? 4 : 0);
+        cp_async4(s + 4u * chunk_off<BK>(r, c), src + (int64_t)r * ld + c, (r < kv && c < cv) ? 4 : 0);
     }
 }
 
@@ -133,26 +144,26 @@ __device__ __forceinline__ void lds(const float* p, float* out) {
 // rows t + i*wg, so the 8 threads of a quarter-warp read 8 consecutive rows
 // (20-float pitch -> 8 distinct 16-byte bank groups) and each fragment read is
 // a float vector of up to 4 K values of one row.
-constexpr int RS = BK + 4;
-
+template <int BK>
 __device__ __forceinline__ void copy_rows(uint32_t s, const float* src, int64_t ld, int log_rows,
                                           int rv, int kv, bool vec, int tid, int nthr) {
+    constexpr int RS = Geo<BK>::RS, TPR = BK / 4, LOG_TPR = BK == 32 ? 3 : 2;
     const int rows = 1 << log_rows;
     if (vec) {
-        const int c0 = (tid & 3) << 2;  // 4 threads per 16-float row
-        const int dr = nthr >> 2;
+        const int c0 = (tid & (TPR - 1)) << 2;  // BK/4 threads per row
+        const int dr = nthr >> LOG_TPR;
         const int kbytes = min(max(kv - c0, 0), 4) * 4;
-        const float* gp = src + (int64_t)(tid >> 2) * ld + c0;
+        const float* gp = src + (int64_t)(tid >> LOG_TPR) * ld + c0;
         const int64_t gstep = (int64_t)dr * ld;
-        for (int r = tid >> 2; r < rows; r += dr) {
+        for (int r = tid >> LOG_TPR; r < rows; r += dr) {
             cp_async16(s + 4u * (r * RS + c0), gp, r < rv ? kbytes : 0);
             gp += gstep;
         }
         return;
     }
-    const int total = rows << LOG_BK;
+    const int total = rows << Geo<BK>::LOG_BK;
     for (int idx = tid; idx < total; idx += nthr) {
-        const int r = idx >> LOG_BK;
+        const int r = idx >> Geo<BK>::LOG_BK;
         const int c = idx & (BK - 1);
         cp_async4(s + 4u * (r * RS + c), src + (int64_t)r * ld + c, (r < rv && c < kv) ? 4 : 0);
     }
@@ -163,8 +174,9 @@ __device__ __forceinline__ void copy_rows(uint32_t s, const float* src, int64_t 
 //   chunk layout:       T >= 4 -> chunks q*wg + t (rows q*4*wg + t*4 + e),
 //                       else rows t*T + i; one T-wide vector per K slice.
 // Offsets are per-thread bases; the K offsets are compile-time immediates.
-template <bool KROW, int T, int ACC>
+template <bool KROW, int T, int ACC, int BK>
 struct Frag {
+    static constexpr int CH = Geo<BK>::CH, RS = Geo<BK>::RS;
     static constexpr int NB = KROW ? T : (T >= 4 ? T / 4 : 1);
     int off[NB];
 
@@ -217,8 +229,9 @@ __device__ __forceinline__ float epilogue(float acc, float alpha, float beta, co
     return beta == 0.0f ? v : fmaf(beta, *c_old, v);
 }
 
-template <int ACC, int RT, int CT, bool TA, bool TB>
+template <int ACC, int RT, int CT, bool TA, bool TB, int BK>
 __global__ void __launch_bounds__(256, 2) simt_gemm_kernel(const Params p) {
+    constexpr int LOG_BK = Geo<BK>::LOG_BK;
     extern __shared__ __align__(16) float smem[];
     const int tid = threadIdx.x;
     const int nthr = p.wgr * p.wgc;
@@ -249,21 +262,21 @@ __global__ void __launch_bounds__(256, 2) simt_gemm_kernel(const Params p) {
         const uint32_t a_dst = sA_u + 4u * stage * p.a_elems;
         const uint32_t b_dst = sB_u + 4u * stage * p.b_elems;
         if constexpr (TA)   // A stored k x m: rows are K
-            copy_direct(a_dst, A + (int64_t)k0 * p.lda + m0, p.lda, p.log_bm, p.M - m0,
+            copy_direct<BK>(a_dst, A + (int64_t)k0 * p.lda + m0, p.lda, p.log_bm, p.M - m0,
                         p.K - k0, p.vecA, tid, nthr);
         else                // A stored m x k: k-contiguous rows, row layout
-            copy_rows(a_dst, A + (int64_t)m0 * p.lda + k0, p.lda, p.log_bm, p.M - m0, p.K - k0,
+            copy_rows<BK>(a_dst, A + (int64_t)m0 * p.lda + k0, p.lda, p.log_bm, p.M - m0, p.K - k0,
                       p.vecA, tid, nthr);
         if constexpr (!TB)  // B stored k x n: rows are K
-            copy_direct(b_dst, B + (int64_t)k0 * p.ldb + n0, p.ldb, p.log_bn, p.N - n0,
+            copy_direct<BK>(b_dst, B + (int64_t)k0 * p.ldb + n0, p.ldb, p.log_bn, p.N - n0,
                         p.K - k0, p.vecB, tid, nthr);
         else                // B stored n x k: k-contiguous rows, row layout
-            copy_rows(b_dst, B + (int64_t)n0 * p.ldb + k0, p.ldb, p.log_bn, p.N - n0, p.K - k0,
+            copy_rows<BK>(b_dst, B + (int64_t)n0 * p.ldb + k0, p.ldb, p.log_bn, p.N - n0, p.K - k0,
                       p.vecB, tid, nthr);
     };
 
-    using FragA = Frag<!TA, RT, ACC>;
-    using FragB = Frag<TB, CT, ACC>;
+    using FragA = Frag<!TA, RT, ACC, BK>;
+    using FragB = Frag<TB, CT, ACC, BK>;
     FragA fa;
     FragB fb;
     fa.init(ty, p.wgr);
@@ -353,20 +366,26 @@ inline int ilog2(int v) {
 }
 inline int round4(int v) { return (v + 3) & ~3; }
 
-// Shared-memory plan for one tile shape (chunk-major operand tiles).
+// Shared-memory plan for one tile shape: K depth, stage count, bytes.
 struct SmemPlan {
-    int a_elems, b_elems, stages;
+    int bk, a_elems, b_elems, stages;
     size_t bytes;
 };
 
 inline SmemPlan plan_smem(bool a_rows, bool b_rows, int bm, int bn) {
-    SmemPlan s;
-    s.a_elems = a_rows ? bm * RS : (round4(bm) / 4) * CH;
-    s.b_elems = b_rows ? bn * RS : (round4(bn) / 4) * CH;
-    const size_t stage = 4u * size_t(s.a_elems + s.b_elems);
-    s.stages = (3 * stage <= 112 * 1024) ? 3 : 2;
-    s.bytes = s.stages * stage;
-    return s;
+    auto make = [&](int bk) {
+        SmemPlan s;
+        s.bk = bk;
+        s.a_elems = a_rows ? bm * (bk + 4) : (round4(bm) / 4) * (bk * 4 + 4);
+        s.b_elems = b_rows ? bn * (bk + 4) : (round4(bn) / 4) * (bk * 4 + 4);
+        const size_t stage = 4u * size_t(s.a_elems + s.b_elems);
+        s.stages = (3 * stage <= 112 * 1024) ? 3 : 2;
+        s.bytes = s.stages * stage;
+        return s;
+    };
+    const SmemPlan deep = make(32);
+    if (deep.bytes <= 112 * 1024) return deep;
+    return make(16);
 }
 
 template <int ACC, int RT, int CT, bool TA, bool TB>
@@ -374,12 +393,13 @@ kp_status launch(const GemmProblem& g, int wgr, int wgc, cudaStream_t stream) {
     const int bm = RT * wgr, bn = CT * wgc;
     const SmemPlan sp = plan_smem(!TA, TB, bm, bn);
     if (sp.bytes > 227 * 1024) return fail(KP_ERR_UNSUPPORTED, "simt: shared-memory plan too large");
-    auto kern = simt_gemm_kernel<ACC, RT, CT, TA, TB>;
-    static bool attr_done = false;  // idempotent; one process drives one device
-    if (!attr_done) {
+    auto kern = sp.bk == 32 ? simt_gemm_kernel<ACC, RT, CT, TA, TB, 32>
+                            : simt_gemm_kernel<ACC, RT, CT, TA, TB, 16>;
+    static bool attr_done[2] = {false, false};  // idempotent; one process drives one device
+    if (!attr_done[sp.bk == 32]) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
             return check_launch("cudaFuncSetAttribute");
-        attr_done = true;
+        attr_done[sp.bk == 32] = true;
     }
     Params p;
     p.A = static_cast<const float*>(g.A);

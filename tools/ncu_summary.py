@@ -116,11 +116,9 @@ def main() -> int:
         if d:
             lines.append(f"| achieved (cold, serialised) | {args.flops / (d * scale) / 1e12:.2f} "
                          f"TFLOP/s |\n")
-    dram = (to_float(m.get("dram_read", ("0", ""))[0]) or 0) + \
-        (to_float(m.get("dram_write", ("0", ""))[0]) or 0)
-    unit = m.get("dram_read", ("", "byte"))[1]
-    mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
-    dram_bytes = dram * mult
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    dram_bytes = sum((to_float(m.get(k, ("0", "byte"))[0]) or 0) *
+                     scale.get(m.get(k, ("0", "byte"))[1], 1) for k in ("dram_read", "dram_write"))
     lines.append(f"| dram traffic | {dram_bytes / 1e6:.2f} MB"
                  + (f" (algorithmic {args.bytes / 1e6:.2f} MB)" if args.bytes else "") + " |\n")
     st = sorted(raw["stalls"].items(), key=lambda kv: -kv[1])[:6]
