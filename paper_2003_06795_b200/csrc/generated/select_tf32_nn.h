@@ -16,605 +16,325 @@ static inline select_tf32_nn_config select_tf32_nn(int64_t m, int64_t k, int64_t
     (void)k;
     (void)n;
     if (m < INT64_C(3584)) {
-        if (n < INT64_C(351)) {
-            if (n < INT64_C(46)) {
+        if (n < INT64_C(2897)) {
+            if (n < INT64_C(111)) {
                 if (m < INT64_C(2218)) {
-                    if (m < INT64_C(1109)) {
+                    if (n < INT64_C(46)) {
                         select_tf32_nn_config out = {1u, 1u, 2u, 8u, 8u};
                         return out;
                     } else {
-                        if (k < INT64_C(167)) {
-                            select_tf32_nn_config out = {1u, 1u, 2u, 8u, 8u};
+                        if (k < INT64_C(272)) {
+                            select_tf32_nn_config out = {1u, 1u, 1u, 8u, 8u};
                             return out;
                         } else {
-                            select_tf32_nn_config out = {2u, 1u, 2u, 8u, 8u};
-                            return out;
+                            if (m < INT64_C(555)) {
+                                if (k < INT64_C(471)) {
+                                    select_tf32_nn_config out = {1u, 1u, 2u, 8u, 8u};
+                                    return out;
+                                } else {
+                                    if (m < INT64_C(278)) {
+                                        select_tf32_nn_config out = {1u, 1u, 2u, 8u, 8u};
+                                        return out;
+                                    } else {
+                                        select_tf32_nn_config out = {4u, 1u, 2u, 16u, 16u};
+                                        return out;
+                                    }
+                                }
+                            } else {
+                                if (m < INT64_C(1109)) {
+                                    if (n < INT64_C(79)) {
+                                        select_tf32_nn_config out = {1u, 1u, 1u, 8u, 8u};
+                                        return out;
+                                    } else {
+                                        select_tf32_nn_config out = {4u, 1u, 2u, 16u, 16u};
+                                        return out;
+                                    }
+                                } else {
+                                    if (k < INT64_C(471)) {
+                                        select_tf32_nn_config out = {1u, 1u, 2u, 8u, 8u};
+                                        return out;
+                                    } else {
+                                        select_tf32_nn_config out = {1u, 1u, 1u, 8u, 8u};
+                                        return out;
+                                    }
+                                }
+                            }
                         }
                     }
                 } else {
-                    select_tf32_nn_config out = {2u, 1u, 2u, 8u, 8u};
-                    return out;
+                    if (n < INT64_C(46)) {
+                        select_tf32_nn_config out = {4u, 1u, 2u, 16u, 16u};
+                        return out;
+                    } else {
+                        if (n < INT64_C(79)) {
+                            select_tf32_nn_config out = {1u, 1u, 1u, 8u, 8u};
+                            return out;
+                        } else {
+                            if (k < INT64_C(471)) {
+                                select_tf32_nn_config out = {4u, 1u, 2u, 16u, 16u};
+                                return out;
+                            } else {
+                                select_tf32_nn_config out = {1u, 1u, 1u, 16u, 16u};
+                                return out;
+                            }
+                        }
+                    }
                 }
             } else {
-                if (m < INT64_C(1109)) {
-                    if (n < INT64_C(222)) {
-                        if (k < INT64_C(1052)) {
-                            if (m < INT64_C(159)) {
-                                if (m < INT64_C(80)) {
-                                    select_tf32_nn_config out = {8u, 1u, 1u, 16u, 16u};
+                if (n < INT64_C(351)) {
+                    if (m < INT64_C(2218)) {
+                        if (m < INT64_C(159)) {
+                            if (k < INT64_C(744)) {
+                                if (m < INT64_C(70)) {
+                                    select_tf32_nn_config out = {1u, 1u, 1u, 8u, 8u};
                                     return out;
                                 } else {
                                     if (m < INT64_C(112)) {
-                                        if (k < INT64_C(744)) {
-                                            select_tf32_nn_config out = {2u, 1u, 2u, 8u, 8u};
-                                            return out;
-                                        } else {
-                                            select_tf32_nn_config out = {4u, 1u, 1u, 8u, 8u};
-                                            return out;
-                                        }
+                                        select_tf32_nn_config out = {4u, 1u, 2u, 16u, 16u};
+                                        return out;
                                     } else {
                                         select_tf32_nn_config out = {1u, 1u, 1u, 8u, 8u};
                                         return out;
                                     }
                                 }
                             } else {
-                                if (n < INT64_C(144)) {
-                                    if (k < INT64_C(444)) {
-                                        if (m < INT64_C(555)) {
-                                            if (m < INT64_C(278)) {
-                                                select_tf32_nn_config out = {8u, 1u, 1u, 16u, 16u};
-                                                return out;
-                                            } else {
-                                                if (n < INT64_C(79)) {
-                                                    select_tf32_nn_config out = {4u, 1u, 1u, 8u, 8u};
-                                                    return out;
-                                                } else {
-                                                    select_tf32_nn_config out = {1u, 1u, 1u, 8u, 8u};
-                                                    return out;
-                                                }
-                                            }
+                                select_tf32_nn_config out = {1u, 1u, 1u, 8u, 8u};
+                                return out;
+                            }
+                        } else {
+                            if (k < INT64_C(744)) {
+                                if (m < INT64_C(317)) {
+                                    if (m < INT64_C(224)) {
+                                        if (k < INT64_C(544)) {
+                                            select_tf32_nn_config out = {1u, 1u, 1u, 16u, 16u};
+                                            return out;
                                         } else {
-                                            select_tf32_nn_config out = {8u, 1u, 1u, 16u, 16u};
+                                            select_tf32_nn_config out = {4u, 1u, 2u, 16u, 16u};
                                             return out;
                                         }
                                     } else {
-                                        if (m < INT64_C(278)) {
-                                            select_tf32_nn_config out = {2u, 1u, 1u, 8u, 8u};
-                                            return out;
-                                        } else {
-                                            if (m < INT64_C(555)) {
-                                                select_tf32_nn_config out = {8u, 1u, 1u, 16u, 16u};
+                                        select_tf32_nn_config out = {1u, 1u, 1u, 8u, 8u};
+                                        return out;
+                                    }
+                                } else {
+                                    if (n < INT64_C(144)) {
+                                        if (m < INT64_C(1109)) {
+                                            if (k < INT64_C(363)) {
+                                                select_tf32_nn_config out = {1u, 1u, 1u, 16u, 16u};
                                                 return out;
                                             } else {
                                                 select_tf32_nn_config out = {1u, 1u, 1u, 8u, 8u};
                                                 return out;
                                             }
-                                        }
-                                    }
-                                } else {
-                                    select_tf32_nn_config out = {8u, 1u, 1u, 16u, 16u};
-                                    return out;
-                                }
-                            }
-                        } else {
-                            select_tf32_nn_config out = {4u, 1u, 1u, 8u, 8u};
-                            return out;
-                        }
-                    } else {
-                        if (k < INT64_C(702)) {
-                            if (k < INT64_C(363)) {
-                                select_tf32_nn_config out = {1u, 1u, 1u, 8u, 8u};
-                                return out;
-                            } else {
-                                select_tf32_nn_config out = {1u, 1u, 1u, 16u, 16u};
-                                return out;
-                            }
-                        } else {
-                            if (m < INT64_C(278)) {
-                                if (k < INT64_C(1536)) {
-                                    if (m < INT64_C(70)) {
-                                        select_tf32_nn_config out = {8u, 1u, 1u, 16u, 16u};
-                                        return out;
-                                    } else {
-                                        if (m < INT64_C(139)) {
-                                            select_tf32_nn_config out = {1u, 1u, 1u, 8u, 8u};
-                                            return out;
                                         } else {
-                                            select_tf32_nn_config out = {8u, 1u, 1u, 16u, 16u};
-                                            return out;
-                                        }
-                                    }
-                                } else {
-                                    select_tf32_nn_config out = {1u, 1u, 1u, 16u, 16u};
-                                    return out;
-                                }
-                            } else {
-                                if (k < INT64_C(992)) {
-                                    if (m < INT64_C(555)) {
-                                        select_tf32_nn_config out = {8u, 1u, 1u, 16u, 16u};
-                                        return out;
-                                    } else {
-                                        select_tf32_nn_config out = {2u, 1u, 1u, 8u, 8u};
-                                        return out;
-                                    }
-                                } else {
-                                    select_tf32_nn_config out = {8u, 1u, 1u, 16u, 16u};
-                                    return out;
-                                }
-                            }
-                        }
-                    }
-                } else {
-                    if (k < INT64_C(1630)) {
-                        if (k < INT64_C(314)) {
-                            if (k < INT64_C(46)) {
-                                if (m < INT64_C(2218)) {
-                                    select_tf32_nn_config out = {8u, 1u, 1u, 16u, 16u};
-                                    return out;
-                                } else {
-                                    select_tf32_nn_config out = {4u, 1u, 1u, 8u, 8u};
-                                    return out;
-                                }
-                            } else {
-                                if (m < INT64_C(2218)) {
-                                    select_tf32_nn_config out = {8u, 1u, 1u, 16u, 16u};
-                                    return out;
-                                } else {
-                                    if (k < INT64_C(111)) {
-                                        select_tf32_nn_config out = {8u, 1u, 1u, 16u, 16u};
-                                        return out;
-                                    } else {
-                                        if (k < INT64_C(222)) {
-                                            select_tf32_nn_config out = {2u, 1u, 2u, 8u, 8u};
-                                            return out;
-                                        } else {
-                                            select_tf32_nn_config out = {8u, 1u, 1u, 16u, 16u};
-                                            return out;
-                                        }
-                                    }
-                                }
-                            }
-                        } else {
-                            if (m < INT64_C(2218)) {
-                                if (n < INT64_C(111)) {
-                                    if (k < INT64_C(471)) {
-                                        if (n < INT64_C(79)) {
-                                            select_tf32_nn_config out = {4u, 1u, 1u, 8u, 8u};
-                                            return out;
-                                        } else {
-                                            select_tf32_nn_config out = {2u, 1u, 2u, 8u, 8u};
-                                            return out;
-                                        }
-                                    } else {
-                                        select_tf32_nn_config out = {4u, 1u, 1u, 8u, 8u};
-                                        return out;
-                                    }
-                                } else {
-                                    if (k < INT64_C(725)) {
-                                        if (n < INT64_C(182)) {
                                             select_tf32_nn_config out = {1u, 1u, 1u, 16u, 16u};
                                             return out;
-                                        } else {
-                                            select_tf32_nn_config out = {8u, 1u, 1u, 16u, 16u};
-                                            return out;
                                         }
                                     } else {
-                                        if (k < INT64_C(1087)) {
-                                            select_tf32_nn_config out = {2u, 1u, 1u, 8u, 8u};
-                                            return out;
-                                        } else {
-                                            select_tf32_nn_config out = {1u, 1u, 1u, 8u, 8u};
-                                            return out;
-                                        }
+                                        select_tf32_nn_config out = {1u, 1u, 1u, 16u, 16u};
+                                        return out;
                                     }
                                 }
                             } else {
-                                if (n < INT64_C(182)) {
-                                    if (n < INT64_C(79)) {
-                                        select_tf32_nn_config out = {1u, 1u, 1u, 8u, 8u};
-                                        return out;
-                                    } else {
-                                        select_tf32_nn_config out = {8u, 1u, 1u, 16u, 16u};
-                                        return out;
-                                    }
-                                } else {
-                                    if (k < INT64_C(1087)) {
-                                        select_tf32_nn_config out = {1u, 1u, 1u, 8u, 8u};
-                                        return out;
-                                    } else {
-                                        select_tf32_nn_config out = {4u, 1u, 1u, 8u, 8u};
-                                        return out;
-                                    }
-                                }
-                            }
-                        }
-                    } else {
-                        select_tf32_nn_config out = {2u, 1u, 2u, 8u, 8u};
-                        return out;
-                    }
-                }
-            }
-        } else {
-            if (m < INT64_C(1268)) {
-                if (k < INT64_C(4345)) {
-                    if (n < INT64_C(544)) {
-                        if (m < INT64_C(139)) {
-                            if (k < INT64_C(1449)) {
-                                select_tf32_nn_config out = {1u, 1u, 1u, 16u, 16u};
-                                return out;
-                            } else {
-                                select_tf32_nn_config out = {1u, 1u, 2u, 8u, 8u};
-                                return out;
-                            }
-                        } else {
-                            if (k < INT64_C(256)) {
-                                if (m < INT64_C(278)) {
+                                if (k < INT64_C(1630)) {
                                     select_tf32_nn_config out = {1u, 1u, 1u, 8u, 8u};
                                     return out;
                                 } else {
                                     select_tf32_nn_config out = {1u, 1u, 1u, 16u, 16u};
                                     return out;
                                 }
-                            } else {
-                                if (m < INT64_C(634)) {
-                                    if (m < INT64_C(278)) {
-                                        if (k < INT64_C(1449)) {
-                                            select_tf32_nn_config out = {2u, 1u, 1u, 8u, 8u};
-                                            return out;
-                                        } else {
-                                            select_tf32_nn_config out = {8u, 1u, 1u, 16u, 16u};
-                                            return out;
-                                        }
-                                    } else {
-                                        select_tf32_nn_config out = {8u, 1u, 1u, 16u, 16u};
-                                        return out;
-                                    }
-                                } else {
-                                    if (k < INT64_C(1449)) {
-                                        select_tf32_nn_config out = {1u, 1u, 1u, 16u, 16u};
-                                        return out;
-                                    } else {
-                                        if (k < INT64_C(2173)) {
-                                            select_tf32_nn_config out = {8u, 1u, 1u, 16u, 16u};
-                                            return out;
-                                        } else {
-                                            select_tf32_nn_config out = {1u, 1u, 1u, 16u, 16u};
-                                            return out;
-                                        }
-                                    }
-                                }
                             }
                         }
                     } else {
-                        if (n < INT64_C(2897)) {
-                            if (m < INT64_C(278)) {
-                                if (k < INT64_C(1620)) {
-                                    if (m < INT64_C(70)) {
-                                        if (m < INT64_C(2)) {
-                                            select_tf32_nn_config out = {4u, 1u, 1u, 8u, 8u};
-                                            return out;
-                                        } else {
-                                            if (n < INT64_C(1620)) {
-                                                if (m < INT64_C(12)) {
-                                                    select_tf32_nn_config out = {2u, 1u, 1u, 8u, 8u};
-                                                    return out;
-                                                } else {
-                                                    if (m < INT64_C(29)) {
+                        if (k < INT64_C(1630)) {
+                            select_tf32_nn_config out = {1u, 1u, 1u, 8u, 8u};
+                            return out;
+                        } else {
+                            select_tf32_nn_config out = {4u, 1u, 2u, 16u, 16u};
+                            return out;
+                        }
+                    }
+                } else {
+                    if (m < INT64_C(2218)) {
+                        if (k < INT64_C(725)) {
+                            if (m < INT64_C(139)) {
+                                select_tf32_nn_config out = {1u, 1u, 1u, 8u, 8u};
+                                return out;
+                            } else {
+                                if (n < INT64_C(1620)) {
+                                    if (k < INT64_C(405)) {
+                                        if (k < INT64_C(111)) {
+                                            if (m < INT64_C(1109)) {
+                                                if (k < INT64_C(79)) {
+                                                    if (m < INT64_C(278)) {
                                                         select_tf32_nn_config out = {1u, 1u, 1u, 8u, 8u};
-                                                        return out;
-                                                    } else {
-                                                        select_tf32_nn_config out = {2u, 1u, 1u, 8u, 8u};
-                                                        return out;
-                                                    }
-                                                }
-                                            } else {
-                                                if (k < INT64_C(725)) {
-                                                    select_tf32_nn_config out = {4u, 1u, 1u, 8u, 8u};
-                                                    return out;
-                                                } else {
-                                                    select_tf32_nn_config out = {2u, 1u, 1u, 8u, 8u};
-                                                    return out;
-                                                }
-                                            }
-                                        }
-                                    } else {
-                                        if (k < INT64_C(203)) {
-                                            if (m < INT64_C(139)) {
-                                                select_tf32_nn_config out = {1u, 1u, 1u, 8u, 8u};
-                                                return out;
-                                            } else {
-                                                select_tf32_nn_config out = {2u, 1u, 1u, 8u, 8u};
-                                                return out;
-                                            }
-                                        } else {
-                                            if (n < INT64_C(1620)) {
-                                                if (n < INT64_C(1145)) {
-                                                    select_tf32_nn_config out = {8u, 1u, 1u, 16u, 16u};
-                                                    return out;
-                                                } else {
-                                                    if (m < INT64_C(139)) {
-                                                        select_tf32_nn_config out = {8u, 1u, 1u, 16u, 16u};
-                                                        return out;
-                                                    } else {
-                                                        select_tf32_nn_config out = {4u, 1u, 1u, 8u, 8u};
-                                                        return out;
-                                                    }
-                                                }
-                                            } else {
-                                                if (m < INT64_C(139)) {
-                                                    if (k < INT64_C(725)) {
-                                                        select_tf32_nn_config out = {2u, 1u, 1u, 8u, 8u};
                                                         return out;
                                                     } else {
                                                         select_tf32_nn_config out = {1u, 1u, 1u, 16u, 16u};
                                                         return out;
                                                     }
                                                 } else {
-                                                    if (k < INT64_C(725)) {
-                                                        select_tf32_nn_config out = {1u, 1u, 2u, 8u, 8u};
-                                                        return out;
-                                                    } else {
-                                                        select_tf32_nn_config out = {8u, 1u, 1u, 16u, 16u};
-                                                        return out;
-                                                    }
-                                                }
-                                            }
-                                        }
-                                    }
-                                } else {
-                                    if (m < INT64_C(2)) {
-                                        select_tf32_nn_config out = {1u, 1u, 1u, 8u, 8u};
-                                        return out;
-                                    } else {
-                                        if (k < INT64_C(2897)) {
-                                            if (m < INT64_C(3)) {
-                                                select_tf32_nn_config out = {1u, 1u, 1u, 16u, 16u};
-                                                return out;
-                                            } else {
-                                                if (m < INT64_C(6)) {
-                                                    select_tf32_nn_config out = {2u, 1u, 2u, 8u, 8u};
+                                                    select_tf32_nn_config out = {1u, 1u, 1u, 8u, 8u};
                                                     return out;
-                                                } else {
-                                                    if (m < INT64_C(12)) {
-                                                        select_tf32_nn_config out = {8u, 1u, 1u, 16u, 16u};
-                                                        return out;
-                                                    } else {
-                                                        select_tf32_nn_config out = {1u, 1u, 1u, 8u, 8u};
-                                                        return out;
-                                                    }
-                                                }
-                                            }
-                                        } else {
-                                            if (m < INT64_C(8)) {
-                                                select_tf32_nn_config out = {4u, 1u, 1u, 8u, 8u};
-                                                return out;
-                                            } else {
-                                                select_tf32_nn_config out = {1u, 1u, 1u, 16u, 16u};
-                                                return out;
-                                            }
-                                        }
-                                    }
-                                }
-                            } else {
-                                if (k < INT64_C(124)) {
-                                    select_tf32_nn_config out = {1u, 1u, 1u, 8u, 8u};
-                                    return out;
-                                } else {
-                                    if (k < INT64_C(725)) {
-                                        if (k < INT64_C(405)) {
-                                            if (m < INT64_C(555)) {
-                                                if (k < INT64_C(203)) {
-                                                    select_tf32_nn_config out = {1u, 1u, 2u, 8u, 8u};
-                                                    return out;
-                                                } else {
-                                                    if (k < INT64_C(287)) {
-                                                        select_tf32_nn_config out = {8u, 1u, 1u, 16u, 16u};
-                                                        return out;
-                                                    } else {
-                                                        select_tf32_nn_config out = {1u, 1u, 1u, 8u, 8u};
-                                                        return out;
-                                                    }
                                                 }
                                             } else {
-                                                if (k < INT64_C(203)) {
+                                                if (k < INT64_C(79)) {
                                                     select_tf32_nn_config out = {1u, 1u, 1u, 8u, 8u};
                                                     return out;
                                                 } else {
-                                                    if (k < INT64_C(287)) {
-                                                        select_tf32_nn_config out = {4u, 1u, 1u, 8u, 8u};
-                                                        return out;
-                                                    } else {
-                                                        select_tf32_nn_config out = {2u, 1u, 1u, 8u, 8u};
-                                                        return out;
-                                                    }
+                                                    select_tf32_nn_config out = {4u, 1u, 2u, 16u, 16u};
+                                                    return out;
                                                 }
                                             }
                                         } else {
-                                            if (n < INT64_C(1449)) {
-                                                select_tf32_nn_config out = {2u, 1u, 2u, 8u, 8u};
+                                            if (m < INT64_C(278)) {
+                                                select_tf32_nn_config out = {1u, 1u, 1u, 16u, 16u};
                                                 return out;
                                             } else {
-                                                select_tf32_nn_config out = {1u, 1u, 2u, 8u, 8u};
-                                                return out;
+                                                if (m < INT64_C(1109)) {
+                                                    if (k < INT64_C(144)) {
+                                                        select_tf32_nn_config out = {1u, 1u, 1u, 16u, 16u};
+                                                        return out;
+                                                    } else {
+                                                        if (m < INT64_C(555)) {
+                                                            if (k < INT64_C(203)) {
+                                                                select_tf32_nn_config out = {1u, 1u, 2u, 8u, 8u};
+                                                                return out;
+                                                            } else {
+                                                                select_tf32_nn_config out = {1u, 1u, 1u, 8u, 8u};
+                                                                return out;
+                                                            }
+                                                        } else {
+                                                            if (k < INT64_C(203)) {
+                                                                select_tf32_nn_config out = {1u, 1u, 1u, 8u, 8u};
+                                                                return out;
+                                                            } else {
+                                                                if (k < INT64_C(287)) {
+                                                                    select_tf32_nn_config out = {4u, 1u, 2u, 16u, 16u};
+                                                                    return out;
+                                                                } else {
+                                                                    select_tf32_nn_config out = {1u, 1u, 2u, 8u, 8u};
+                                                                    return out;
+                                                                }
+                                                            }
+                                                        }
+                                                    }
+                                                } else {
+                                                    select_tf32_nn_config out = {1u, 1u, 2u, 8u, 8u};
+                                                    return out;
+                                                }
                                             }
                                         }
                                     } else {
-                                        if (m < INT64_C(555)) {
-                                            select_tf32_nn_config out = {1u, 1u, 1u, 8u, 8u};
-                                            return out;
-                                        } else {
-                                            if (m < INT64_C(896)) {
-                                                select_tf32_nn_config out = {2u, 1u, 2u, 8u, 8u};
+                                        select_tf32_nn_config out = {1u, 1u, 1u, 8u, 8u};
+                                        return out;
+                                    }
+                                } else {
+                                    select_tf32_nn_config out = {1u, 1u, 2u, 8u, 8u};
+                                    return out;
+                                }
+                            }
+                        } else {
+                            if (k < INT64_C(2173)) {
+                                if (m < INT64_C(6)) {
+                                    select_tf32_nn_config out = {1u, 1u, 1u, 16u, 16u};
+                                    return out;
+                                } else {
+                                    if (m < INT64_C(29)) {
+                                        if (m < INT64_C(12)) {
+                                            if (k < INT64_C(1620)) {
+                                                select_tf32_nn_config out = {1u, 1u, 2u, 8u, 8u};
                                                 return out;
                                             } else {
                                                 select_tf32_nn_config out = {1u, 1u, 1u, 8u, 8u};
                                                 return out;
                                             }
-                                        }
-                                    }
-                                }
-                            }
-                        } else {
-                            if (m < INT64_C(12)) {
-                                select_tf32_nn_config out = {2u, 1u, 2u, 8u, 8u};
-                                return out;
-                            } else {
-                                select_tf32_nn_config out = {2u, 1u, 1u, 8u, 8u};
-                                return out;
-                            }
-                        }
-                    }
-                } else {
-                    if (m < INT64_C(70)) {
-                        select_tf32_nn_config out = {8u, 1u, 1u, 16u, 16u};
-                        return out;
-                    } else {
-                        if (m < INT64_C(139)) {
-                            select_tf32_nn_config out = {2u, 1u, 2u, 8u, 8u};
-                            return out;
-                        } else {
-                            if (m < INT64_C(278)) {
-                                select_tf32_nn_config out = {8u, 1u, 1u, 16u, 16u};
-                                return out;
-                            } else {
-                                if (m < INT64_C(555)) {
-                                    select_tf32_nn_config out = {1u, 1u, 1u, 8u, 8u};
-                                    return out;
-                                } else {
-                                    select_tf32_nn_config out = {8u, 1u, 1u, 16u, 16u};
-                                    return out;
-                                }
-                            }
-                        }
-                    }
-                }
-            } else {
-                if (m < INT64_C(2218)) {
-                    if (n < INT64_C(544)) {
-                        if (k < INT64_C(91)) {
-                            select_tf32_nn_config out = {2u, 1u, 1u, 8u, 8u};
-                            return out;
-                        } else {
-                            if (k < INT64_C(544)) {
-                                select_tf32_nn_config out = {1u, 1u, 2u, 8u, 8u};
-                                return out;
-                            } else {
-                                select_tf32_nn_config out = {4u, 1u, 1u, 8u, 8u};
-                                return out;
-                            }
-                        }
-                    } else {
-                        select_tf32_nn_config out = {2u, 1u, 2u, 8u, 8u};
-                        return out;
-                    }
-                } else {
-                    if (k < INT64_C(1087)) {
-                        if (k < INT64_C(182)) {
-                            if (k < INT64_C(111)) {
-                                select_tf32_nn_config out = {1u, 1u, 2u, 8u, 8u};
-                                return out;
-                            } else {
-                                select_tf32_nn_config out = {2u, 1u, 2u, 8u, 8u};
-                                return out;
-                            }
-                        } else {
-                            select_tf32_nn_config out = {1u, 1u, 2u, 8u, 8u};
-                            return out;
-                        }
-                    } else {
-                        select_tf32_nn_config out = {2u, 1u, 2u, 8u, 8u};
-                        return out;
-                    }
-                }
-            }
-        }
-    } else {
-        if (k < INT64_C(815)) {
-            if (n < INT64_C(46)) {
-                if (m < INT64_C(35480)) {
-                    if (m < INT64_C(8870)) {
-                        if (k < INT64_C(118)) {
-                            select_tf32_nn_config out = {1u, 1u, 2u, 8u, 8u};
-                            return out;
-                        } else {
-                            select_tf32_nn_config out = {1u, 1u, 1u, 16u, 16u};
-                            return out;
-                        }
-                    } else {
-                        if (k < INT64_C(63)) {
-                            select_tf32_nn_config out = {2u, 1u, 1u, 8u, 8u};
-                            return out;
-                        } else {
-                            if (k < INT64_C(167)) {
-                                select_tf32_nn_config out = {8u, 1u, 1u, 16u, 16u};
-                                return out;
-                            } else {
-                                select_tf32_nn_config out = {2u, 1u, 1u, 8u, 8u};
-                                return out;
-                            }
-                        }
-                    }
-                } else {
-                    if (m < INT64_C(70960)) {
-                        if (k < INT64_C(30)) {
-                            select_tf32_nn_config out = {1u, 1u, 2u, 8u, 8u};
-                            return out;
-                        } else {
-                            select_tf32_nn_config out = {1u, 1u, 1u, 8u, 8u};
-                            return out;
-                        }
-                    } else {
-                        select_tf32_nn_config out = {1u, 1u, 1u, 8u, 8u};
-                        return out;
-                    }
-                }
-            } else {
-                if (m < INT64_C(17740)) {
-                    if (n < INT64_C(222)) {
-                        if (n < INT64_C(91)) {
-                            if (m < INT64_C(8870)) {
-                                select_tf32_nn_config out = {8u, 1u, 1u, 16u, 16u};
-                                return out;
-                            } else {
-                                if (k < INT64_C(194)) {
-                                    if (k < INT64_C(97)) {
-                                        select_tf32_nn_config out = {4u, 1u, 1u, 8u, 8u};
-                                        return out;
-                                    } else {
-                                        select_tf32_nn_config out = {2u, 1u, 2u, 8u, 8u};
-                                        return out;
-                                    }
-                                } else {
-                                    select_tf32_nn_config out = {4u, 1u, 1u, 8u, 8u};
-                                    return out;
-                                }
-                            }
-                        } else {
-                            if (k < INT64_C(91)) {
-                                select_tf32_nn_config out = {2u, 1u, 2u, 8u, 8u};
-                                return out;
-                            } else {
-                                if (m < INT64_C(8870)) {
-                                    if (k < INT64_C(363)) {
-                                        select_tf32_nn_config out = {2u, 1u, 1u, 8u, 8u};
-                                        return out;
-                                    } else {
-                                        select_tf32_nn_config out = {2u, 1u, 2u, 8u, 8u};
-                                        return out;
-                                    }
-                                } else {
-                                    if (k < INT64_C(363)) {
-                                        select_tf32_nn_config out = {2u, 1u, 2u, 8u, 8u};
-                                        return out;
-                                    } else {
-                                        if (k < INT64_C(544)) {
+                                        } else {
                                             select_tf32_nn_config out = {1u, 1u, 1u, 8u, 8u};
                                             return out;
+                                        }
+                                    } else {
+                                        if (m < INT64_C(896)) {
+                                            if (n < INT64_C(1024)) {
+                                                if (k < INT64_C(1449)) {
+                                                    select_tf32_nn_config out = {1u, 1u, 1u, 16u, 16u};
+                                                    return out;
+                                                } else {
+                                                    if (m < INT64_C(99)) {
+                                                        select_tf32_nn_config out = {1u, 1u, 2u, 8u, 8u};
+                                                        return out;
+                                                    } else {
+                                                        if (m < INT64_C(393)) {
+                                                            select_tf32_nn_config out = {1u, 1u, 1u, 8u, 8u};
+                                                            return out;
+                                                        } else {
+                                                            select_tf32_nn_config out = {1u, 1u, 1u, 16u, 16u};
+                                                            return out;
+                                                        }
+                                                    }
+                                                }
+                                            } else {
+                                                if (m < INT64_C(139)) {
+                                                    select_tf32_nn_config out = {1u, 1u, 1u, 16u, 16u};
+                                                    return out;
+                                                } else {
+                                                    if (m < INT64_C(278)) {
+                                                        select_tf32_nn_config out = {1u, 1u, 2u, 8u, 8u};
+                                                        return out;
+                                                    } else {
+                                                        if (m < INT64_C(555)) {
+                                                            select_tf32_nn_config out = {4u, 1u, 2u, 16u, 16u};
+                                                            return out;
+                                                        } else {
+                                                            select_tf32_nn_config out = {1u, 1u, 2u, 8u, 8u};
+                                                            return out;
+                                                        }
+                                                    }
+                                                }
+                                            }
                                         } else {
-                                            select_tf32_nn_config out = {2u, 1u, 2u, 8u, 8u};
+                                            select_tf32_nn_config out = {1u, 1u, 1u, 8u, 8u};
                                             return out;
                                         }
                                     }
+                                }
+                            } else {
+                                if (m < INT64_C(555)) {
+                                    if (m < INT64_C(2)) {
+                                        select_tf32_nn_config out = {1u, 1u, 1u, 8u, 8u};
+                                        return out;
+                                    } else {
+                                        if (m < INT64_C(278)) {
+                                            if (m < INT64_C(70)) {
+                                                if (m < INT64_C(3)) {
+                                                    select_tf32_nn_config out = {1u, 1u, 2u, 8u, 8u};
+                                                    return out;
+                                                } else {
+                                                    if (m < INT64_C(8)) {
+                                                        select_tf32_nn_config out = {1u, 1u, 1u, 8u, 8u};
+                                                        return out;
+                                                    } else {
+                                                        if (m < INT64_C(29)) {
+                                                            select_tf32_nn_config out = {1u, 1u, 1u, 16u, 16u};
+                                                            return out;
+                                                        } else {
+                                                            select_tf32_nn_config out = {4u, 1u, 2u, 16u, 16u};
+                                                            return out;
+                                                        }
+                                                    }
+                                                }
+                                            } else {
+                                                select_tf32_nn_config out = {1u, 1u, 2u, 8u, 8u};
+                                                return out;
+                                            }
+                                        } else {
+                                            select_tf32_nn_config out = {1u, 1u, 1u, 8u, 8u};
+                                            return out;
+                                        }
+                                    }
+                                } else {
+                                    select_tf32_nn_config out = {4u, 1u, 2u, 16u, 16u};
+                                    return out;
                                 }
                             }
                         }
@@ -622,83 +342,113 @@ static inline select_tf32_nn_config select_tf32_nn(int64_t m, int64_t k, int64_t
                         select_tf32_nn_config out = {1u, 1u, 2u, 8u, 8u};
                         return out;
                     }
+                }
+            }
+        } else {
+            select_tf32_nn_config out = {4u, 1u, 2u, 16u, 16u};
+            return out;
+        }
+    } else {
+        if (n < INT64_C(28)) {
+            if (m < INT64_C(8870)) {
+                if (k < INT64_C(118)) {
+                    select_tf32_nn_config out = {4u, 1u, 2u, 16u, 16u};
+                    return out;
                 } else {
+                    select_tf32_nn_config out = {1u, 1u, 1u, 16u, 16u};
+                    return out;
+                }
+            } else {
+                if (m < INT64_C(141920)) {
+                    select_tf32_nn_config out = {1u, 1u, 1u, 8u, 8u};
+                    return out;
+                } else {
+                    select_tf32_nn_config out = {1u, 1u, 2u, 8u, 8u};
+                    return out;
+                }
+            }
+        } else {
+            if (n < INT64_C(79)) {
+                if (m < INT64_C(17740)) {
                     if (k < INT64_C(384)) {
-                        if (m < INT64_C(35480)) {
-                            if (n < INT64_C(79)) {
-                                if (k < INT64_C(97)) {
-                                    select_tf32_nn_config out = {2u, 1u, 2u, 8u, 8u};
-                                    return out;
-                                } else {
-                                    select_tf32_nn_config out = {1u, 1u, 2u, 8u, 8u};
-                                    return out;
-                                }
+                        if (k < INT64_C(146)) {
+                            if (k < INT64_C(42)) {
+                                select_tf32_nn_config out = {4u, 1u, 2u, 16u, 16u};
+                                return out;
                             } else {
-                                select_tf32_nn_config out = {1u, 1u, 2u, 8u, 8u};
+                                select_tf32_nn_config out = {1u, 1u, 1u, 8u, 8u};
                                 return out;
                             }
+                        } else {
+                            if (m < INT64_C(8870)) {
+                                select_tf32_nn_config out = {1u, 1u, 1u, 16u, 16u};
+                                return out;
+                            } else {
+                                if (n < INT64_C(46)) {
+                                    select_tf32_nn_config out = {1u, 1u, 1u, 16u, 16u};
+                                    return out;
+                                } else {
+                                    select_tf32_nn_config out = {4u, 1u, 2u, 16u, 16u};
+                                    return out;
+                                }
+                            }
+                        }
+                    } else {
+                        if (m < INT64_C(8870)) {
+                            select_tf32_nn_config out = {1u, 1u, 1u, 8u, 8u};
+                            return out;
                         } else {
                             select_tf32_nn_config out = {1u, 1u, 2u, 8u, 8u};
                             return out;
                         }
-                    } else {
-                        if (n < INT64_C(91)) {
-                            if (m < INT64_C(35480)) {
-                                select_tf32_nn_config out = {2u, 1u, 2u, 8u, 8u};
-                                return out;
-                            } else {
-                                if (m < INT64_C(567677)) {
-                                    select_tf32_nn_config out = {1u, 1u, 2u, 8u, 8u};
-                                    return out;
-                                } else {
-                                    select_tf32_nn_config out = {2u, 1u, 2u, 8u, 8u};
-                                    return out;
-                                }
-                            }
-                        } else {
-                            if (m < INT64_C(35480)) {
-                                select_tf32_nn_config out = {1u, 1u, 2u, 8u, 8u};
-                                return out;
-                            } else {
-                                select_tf32_nn_config out = {4u, 1u, 8u, 16u, 16u};
-                                return out;
-                            }
-                        }
-                    }
-                }
-            }
-        } else {
-            if (n < INT64_C(363)) {
-                if (m < INT64_C(35480)) {
-                    if (m < INT64_C(8870)) {
-                        select_tf32_nn_config out = {2u, 1u, 2u, 8u, 8u};
-                        return out;
-                    } else {
-                        if (k < INT64_C(1630)) {
-                            if (m < INT64_C(17740)) {
-                                if (n < INT64_C(182)) {
-                                    select_tf32_nn_config out = {2u, 1u, 2u, 8u, 8u};
-                                    return out;
-                                } else {
-                                    select_tf32_nn_config out = {1u, 1u, 2u, 8u, 8u};
-                                    return out;
-                                }
-                            } else {
-                                select_tf32_nn_config out = {1u, 1u, 2u, 8u, 8u};
-                                return out;
-                            }
-                        } else {
-                            select_tf32_nn_config out = {4u, 1u, 8u, 16u, 16u};
-                            return out;
-                        }
                     }
                 } else {
-                    select_tf32_nn_config out = {4u, 1u, 8u, 16u, 16u};
-                    return out;
+                    if (m < INT64_C(141920)) {
+                        select_tf32_nn_config out = {1u, 1u, 2u, 8u, 8u};
+                        return out;
+                    } else {
+                        if (k < INT64_C(63)) {
+                            select_tf32_nn_config out = {1u, 1u, 2u, 8u, 8u};
+                            return out;
+                        } else {
+                            if (m < INT64_C(567677)) {
+                                select_tf32_nn_config out = {4u, 1u, 2u, 16u, 16u};
+                                return out;
+                            } else {
+                                select_tf32_nn_config out = {1u, 1u, 2u, 8u, 8u};
+                                return out;
+                            }
+                        }
+                    }
                 }
             } else {
-                select_tf32_nn_config out = {4u, 1u, 8u, 16u, 16u};
-                return out;
+                if (k < INT64_C(46)) {
+                    if (m < INT64_C(8870)) {
+                        select_tf32_nn_config out = {4u, 1u, 2u, 16u, 16u};
+                        return out;
+                    } else {
+                        select_tf32_nn_config out = {1u, 1u, 2u, 8u, 8u};
+                        return out;
+                    }
+                } else {
+                    if (k < INT64_C(544)) {
+                        if (k < INT64_C(363)) {
+                            select_tf32_nn_config out = {1u, 1u, 2u, 8u, 8u};
+                            return out;
+                        } else {
+                            if (m < INT64_C(8870)) {
+                                select_tf32_nn_config out = {1u, 1u, 2u, 8u, 8u};
+                                return out;
+                            } else {
+                                select_tf32_nn_config out = {1u, 1u, 1u, 8u, 8u};
+                                return out;
+                            }
+                        }
+                    } else {
+                        select_tf32_nn_config out = {1u, 1u, 2u, 8u, 8u};
+                        return out;
+                    }
+                }
             }
         }
     }

@@ -25,7 +25,8 @@
 //   wg     (16, 16)   -> persistent CTAs (grid = SM count), double-buffered
 //                        TMEM accumulator: epilogue of tile i overlaps the
 //                        MMAs of tile i+1
-// 32 configs per family, canonical KernelConfig order.
+//   row_tile 2        -> CTA pair, cta_group::2, M = 256 (persistent, ct 4|8)
+// 40 configs per family, canonical KernelConfig order.
 #include <cuda.h>
 
 #include <algorithm>
@@ -376,6 +377,237 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     }
 }
 
+// --------------------------------------------------------- 2-CTA kernel
+// cta_group::2: a cluster of two CTAs (one TPC) computes a 256 x BN tile with
+// M=256 tcgen05.mma issued by the even (leader) CTA. Each CTA stages its own
+// 128 rows of A and half (BN/2) of B per stage -- the pair shares operands, so
+// shared-memory fill traffic per MMA flop is 2/3 of the 1-CTA kernel's at
+// BN = 256 -- and holds its 128 x BN half of D in its own TMEM. Both CTAs'
+// TMA transactions complete on the leader's full barrier; the leader's
+// tcgen05.commit multicasts to both CTAs' empty / acc_full barriers; both
+// epilogues release the leader's acc_empty barrier. Persistent over tiles
+// with a double-buffered accumulator, like the NBUF = 2 kernel.
+__device__ __forceinline__ void tma_load_3d_pair(uint32_t dst, const CUtensorMap* map, int c0,
+                                                 int c1, int c2, uint32_t leader_bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];"
+        :: "r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2),
+           "r"(leader_bar) : "memory");
+}
+__device__ __forceinline__ void umma_commit_pair(uint32_t bar) {
+    asm volatile(
+        "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], m;\n\t}" :: "r"(bar) : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
+                 ::: "memory");
+}
+template <int ES>
+__device__ __forceinline__ void mma_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t accumulate) {
+    if constexpr (ES == 4) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
+            :: "r"(tmem_d), "l"(a), "l"(b), "r"(idesc), "r"(accumulate) : "memory");
+    } else {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+            :: "r"(tmem_d), "l"(a), "l"(b), "r"(idesc), "r"(accumulate) : "memory");
+    }
+}
+
+constexpr uint32_t PEER_MASK = 0xFEFFFFFFu;  // shared::cluster address of the even CTA
+
+template <int ES, int BN, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap map_a,
+                    const __grid_constant__ CUtensorMap map_b, const TcParams p) {
+    constexpr int ROW = 128;
+    constexpr int BK = ROW / ES;
+    constexpr int UMMA_K = 32 / ES;
+    constexpr int HN = BN / 2;                   // B columns staged per CTA
+    using MA = MnMajor<ES, BM>;
+    using MB = MnMajor<ES, HN>;
+    constexpr uint32_t A_BYTES = BM * ROW;
+    constexpr uint32_t B_BYTES = HN * ROW;
+    constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+    // M = 256 across the pair, N = BN
+    constexpr uint32_t IDESC =
+        (instr_desc<ES, A_MN, B_MN, BN>() & ~(0x1Fu << 24)) | (uint32_t(256 >> 4) << 24);
+    constexpr uint32_t TMEM_COLS = 2 * BN;
+
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + STAGE_ALIGN - 1) & ~uint32_t(STAGE_ALIGN - 1);
+    uint8_t* gbase = smem_raw + (base - raw);
+    const int S = p.stages;
+    const uint32_t bars = base + S * STAGE_BYTES;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + S * STAGE_BYTES + (2 * S + 4) * 8);
+    float* staging = reinterpret_cast<float*>(gbase + S * STAGE_BYTES + (2 * S + 5) * 8);
+    auto full_bar = [&](int s) { return bars + 8u * s; };
+    auto empty_bar = [&](int s) { return bars + 8u * (S + s); };
+    auto acc_full = [&](int b) { return bars + 8u * (2 * S + b); };
+    auto acc_empty = [&](int b) { return bars + 8u * (2 * S + 2 + b); };
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    uint32_t rank;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    const bool leader = rank == 0;
+    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+    // pair tiles: 256-row m tiles (tiles_m counts them)
+    const int total = p.tiles_m * p.tiles_n * p.batch;
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(full_bar(s), 1);
+            mbar_init(empty_bar(s), 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(acc_full(b), 1);
+            mbar_init(acc_empty(b), 8);  // 4 epilogue warps x 2 CTAs
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;"
+                     :: "r"(smem_u32(tmem_slot)), "r"(TMEM_COLS) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    fence_before_sync();
+    cluster_sync();  // both CTAs' barriers exist before any remote arrive / multicast
+    fence_after_sync();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---- TMA producer (both CTAs; bytes land on the leader's barrier)
+            int kt_all = 0;
+            for (int t = pair; t < total; t += npairs) {
+                int m0, n0, bz;
+                tile_coords(t, p, BN, m0, n0, bz);  // m0 in units of BM*2 below
+                m0 = m0 * 2 + int(rank) * BM;
+                const int nb = n0 + int(rank) * HN;
+                const int za = bz * p.a_batch, zb = bz * p.b_batch;
+                for (int kt = 0; kt < p.k_tiles; ++kt, ++kt_all) {
+                    const int s = kt_all % S;
+                    const uint32_t phase = (kt_all / S) & 1;
+                    mbar_wait(empty_bar(s), phase ^ 1);
+                    const uint32_t lbar = full_bar(s) & PEER_MASK;
+                    if (leader) mbar_expect_tx(full_bar(s), 2 * STAGE_BYTES);
+                    const uint32_t sa = base + s * STAGE_BYTES;
+                    const uint32_t sb = sa + A_BYTES;
+                    const int k0 = kt * BK;
+                    if constexpr (!A_MN) {
+                        tma_load_3d_pair(sa, &map_a, k0, m0, za, lbar);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < BM / MA::ATOM; ++j)
+                            tma_load_3d_pair(sa + j * BK * MA::W, &map_a, m0 + j * MA::ATOM, k0, za,
+                                             lbar);
+                    }
+                    if constexpr (!B_MN) {
+                        tma_load_3d_pair(sb, &map_b, k0, nb, zb, lbar);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < HN / MB::ATOM; ++j)
+                            tma_load_3d_pair(sb + j * BK * MB::W, &map_b, nb + j * MB::ATOM, k0, zb,
+                                             lbar);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && leader) {  // ---- MMA issuer (leader only)
+            int kt_all = 0, it = 0;
+            for (int t = pair; t < total; t += npairs, ++it) {
+                const int buf = it & 1;
+                const uint32_t use = (it >> 1) & 1;
+                mbar_wait(acc_empty(buf), use ^ 1);
+                fence_after_sync();
+                const uint32_t d = tmem + uint32_t(buf * BN);
+                for (int kt = 0; kt < p.k_tiles; ++kt, ++kt_all) {
+                    const int s = kt_all % S;
+                    const uint32_t phase = (kt_all / S) & 1;
+                    mbar_wait(full_bar(s), phase);
+                    fence_after_sync();
+                    const uint32_t sa = base + s * STAGE_BYTES;
+                    const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+                    for (int k = 0; k < BK / UMMA_K; ++k) {
+                        const uint64_t da =
+                            A_MN ? smem_desc(sa + k * UMMA_K * MA::W, BK * MA::W, MA::SBO, MA::LAYOUT)
+                                 : smem_desc(sa + k * 32, 16, 1024, 2);
+                        const uint64_t db =
+                            B_MN ? smem_desc(sb + k * UMMA_K * MB::W, BK * MB::W, MB::SBO, MB::LAYOUT)
+                                 : smem_desc(sb + k * 32, 16, 1024, 2);
+                        mma_pair<ES>(d, da, db, IDESC, (kt | k) != 0);
+                    }
+                    umma_commit_pair(empty_bar(s));   // frees stage s in both CTAs
+                }
+                umma_commit_pair(acc_full(buf));      // both halves of D complete
+            }
+        }
+    } else {  // ---- epilogue warps 2..5 of both CTAs: own 128 rows of D
+        const int q = warp & 3;
+        float* st = staging + (warp - 2) * 32 * EPI_PITCH;
+        int it = 0;
+        for (int t = pair; t < total; t += npairs, ++it) {
+            int m0, n0, bz;
+            tile_coords(t, p, BN, m0, n0, bz);
+            m0 = m0 * 2 + int(rank) * BM;
+            const int buf = it & 1;
+            const uint32_t use = (it >> 1) & 1;
+            mbar_wait(acc_full(buf), use);
+            fence_after_sync();
+            float* Cb = p.C + int64_t(bz) * p.sc;
+            const int row0 = m0 + q * 32;
+            const uint32_t taddr = tmem + (uint32_t(q * 32) << 16) + uint32_t(buf * BN);
+            const int cols = min(BN, p.N - n0);
+#pragma unroll 1
+            for (int c0 = 0; c0 < cols; c0 += 32) {
+                float v[32];
+                tmem_ld32(taddr + c0, v);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) st[lane * EPI_PITCH + j] = v[j];
+                __syncwarp();
+                const int n = n0 + c0 + lane;
+                if (n < p.N) {
+#pragma unroll 4
+                    for (int r = 0; r < 32; ++r) {
+                        const int m = row0 + r;
+                        if (m < p.M) {
+                            float* dst = Cb + int64_t(m) * p.ldc + n;
+                            const float x = p.alpha * st[r * EPI_PITCH + lane];
+                            *dst = p.beta == 0.0f ? x : fmaf(p.beta, *dst, x);
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+            fence_before_sync();
+            if (lane == 0) {
+                asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];"
+                             :: "r"(acc_empty(buf) & PEER_MASK) : "memory");
+            }
+        }
+    }
+    fence_before_sync();
+    __syncthreads();
+    cluster_sync();
+    if (warp == 1) {
+        fence_after_sync();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" :: "r"(tmem),
+                     "r"(TMEM_COLS) : "memory");
+    }
+}
+
 // ------------------------------------------------------------------- host
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                               const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -421,25 +653,41 @@ static int tidx(uint32_t v) {
     return -1;
 }
 
-// Config list per family: acc x col_tile x {wg (8,8): one tile per CTA,
-// wg (16,16): persistent CTAs with a double-buffered TMEM accumulator}.
-int32_t num_configs(kp_family fam) { return (fam == KP_TF32_TC || fam == KP_BF16_TC) ? 32 : 0; }
+// Config list per family (canonical KernelConfig order):
+//   (acc, 1, ct, 8, 8)    one 128 x BN tile per CTA
+//   (acc, 1, ct, 16, 16)  persistent CTAs, double-buffered TMEM accumulator
+//   (acc, 2, ct, 16, 16)  persistent CTA pairs (cta_group::2, M = 256), ct in {4, 8}
+static int tc_config_table(kp_config* out) {
+    int n = 0;
+    for (int a = 0; a < 4; ++a) {
+        for (int c = 0; c < 4; ++c) {
+            out[n++] = kp_config{kTiles[a], 1u, kTiles[c], 8u, 8u};
+            out[n++] = kp_config{kTiles[a], 1u, kTiles[c], 16u, 16u};
+        }
+        for (int c = 2; c < 4; ++c) out[n++] = kp_config{kTiles[a], 2u, kTiles[c], 16u, 16u};
+    }
+    return n;
+}
+
+int32_t num_configs(kp_family fam) { return (fam == KP_TF32_TC || fam == KP_BF16_TC) ? 40 : 0; }
 
 kp_status config_at(kp_family fam, int32_t index, kp_config* out) {
     if (index < 0 || index >= num_configs(fam)) return fail(KP_ERR_INVALID_ARG, "config index out of range");
-    const uint32_t wg = (index % 2) ? 16u : 8u;
-    *out = kp_config{kTiles[index / 8], 1u, kTiles[(index / 2) % 4], wg, wg};
+    kp_config table[40];
+    tc_config_table(table);
+    *out = table[index];
     return KP_OK;
 }
 
 kp_status valid(kp_family fam, const kp_config& c) {
     if (num_configs(fam) == 0) return fail(KP_ERR_INVALID_ARG, "not a tensor-core family");
-    const bool wg_ok = (c.wg_rows == 8 && c.wg_cols == 8) || (c.wg_rows == 16 && c.wg_cols == 16);
-    if (tidx(c.acc) < 0 || c.row_tile != 1 || tidx(c.col_tile) < 0 || !wg_ok)
-        return fail(KP_ERR_INVALID_CONFIG,
-                    "tcgen05 family configs are (acc in 1,2,4,8; row_tile 1; col_tile in 1,2,4,8; "
-                    "wg 8x8 or 16x16)");
-    return KP_OK;
+    kp_config table[40];
+    const int n = tc_config_table(table);
+    for (int i = 0; i < n; ++i)
+        if (std::memcmp(&table[i], &c, sizeof c) == 0) return KP_OK;
+    return fail(KP_ERR_INVALID_CONFIG,
+                "tcgen05 family configs: (acc, 1, ct, 8, 8), (acc, 1, ct, 16, 16), "
+                "(acc, 2, ct in 4|8, 16, 16); acc, ct in 1,2,4,8");
 }
 
 static size_t smem_bytes(int bn, int stages) {
@@ -504,6 +752,86 @@ static kp_status launch_t(const GemmProblem& g, int want_stages, cudaStream_t st
     return check_launch("tc_gemm_kernel");
 }
 
+static size_t pair_smem_bytes(int bn, int stages) {
+    return STAGE_ALIGN + size_t(stages) * (BM + bn / 2) * 128 + (2 * stages + 6) * 8 +
+           4 * 32 * EPI_PITCH * 4;
+}
+
+template <int ES, int BN, bool A_MN, bool B_MN>
+static kp_status launch_pair(const GemmProblem& g, int want_stages, cudaStream_t stream) {
+    int stages = want_stages;
+    while (stages > 2 && pair_smem_bytes(BN, stages) > 227 * 1024) --stages;
+    const size_t smem = pair_smem_bytes(BN, stages);
+    const bool bf16 = ES == 2;
+    const int BK = 128 / ES;
+    constexpr int HN = BN / 2;
+    CUtensorMap ma, mb;
+    kp_status st;
+    const int64_t bat_a = g.sa ? g.batch : 1, bat_b = g.sb ? g.batch : 1;
+    using MA = MnMajor<ES, BM>;
+    using MB = MnMajor<ES, HN>;
+    const int sw128 = int(CU_TENSOR_MAP_SWIZZLE_128B);
+    if (!A_MN) st = make_map(&ma, bf16, g.A, g.k, g.m, bat_a, g.lda, g.sa, BK, BM, sw128);
+    else       st = make_map(&ma, bf16, g.A, g.m, g.k, bat_a, g.lda, g.sa, MA::ATOM, BK, MA::TMA_SWIZZLE);
+    if (st != KP_OK) return st;
+    if (!B_MN) st = make_map(&mb, bf16, g.B, g.k, g.n, bat_b, g.ldb, g.sb, BK, HN, sw128);
+    else       st = make_map(&mb, bf16, g.B, g.n, g.k, bat_b, g.ldb, g.sb, MB::ATOM, BK, MB::TMA_SWIZZLE);
+    if (st != KP_OK) return st;
+    auto kern = tc_gemm_pair_kernel<ES, BN, A_MN, B_MN>;
+    static bool attr_done = false;
+    if (!attr_done) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
+            return check_launch("cudaFuncSetAttribute");
+        attr_done = true;
+    }
+    TcParams p;
+    p.C = g.C;
+    p.M = int(g.m); p.N = int(g.n); p.K = int(g.k);
+    p.ldc = g.ldc; p.sc = g.sc;
+    p.alpha = g.alpha; p.beta = g.beta;
+    p.tiles_m = int((g.m + 2 * BM - 1) / (2 * BM));  // 256-row pair tiles
+    p.tiles_n = int((g.n + BN - 1) / BN);
+    p.stages = stages;
+    p.k_tiles = int((g.k + BK - 1) / BK);
+    p.batch = int(g.batch);
+    p.a_batch = g.sa ? 1 : 0;
+    p.b_batch = g.sb ? 1 : 0;
+    const int64_t tiles = int64_t(p.tiles_m) * p.tiles_n * g.batch;
+    if (tiles > 0x3fffffffLL) return fail(KP_ERR_BAD_SHAPE, "tc: grid too large");
+    const int64_t pairs = std::min<int64_t>(tiles, sm_count() / 2);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(2 * pairs));
+    cfg.blockDim = dim3(NUM_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, kern, ma, mb, p) != cudaSuccess) return check_launch("tc_gemm_pair_kernel");
+    note_launch();
+    return check_launch("tc_gemm_pair_kernel");
+}
+
+template <int ES, int BN>
+static kp_status by_layout_pair(const GemmProblem& g, int stages, cudaStream_t s) {
+    if (!g.ta && g.tb) return launch_pair<ES, BN, false, false>(g, stages, s);
+    if (!g.ta && !g.tb) return launch_pair<ES, BN, false, true>(g, stages, s);
+    if (g.ta && g.tb) return launch_pair<ES, BN, true, false>(g, stages, s);
+    return launch_pair<ES, BN, true, true>(g, stages, s);
+}
+
+template <int ES>
+static kp_status by_tile_pair(const kp_config& c, const GemmProblem& g, cudaStream_t s) {
+    static const int kStages[4] = {2, 3, 4, 6};
+    const int stages = kStages[tidx(c.acc)];
+    if (c.col_tile == 4) return by_layout_pair<ES, 128>(g, stages, s);
+    return by_layout_pair<ES, 256>(g, stages, s);
+}
+
 template <int ES, int BN, int NBUF>
 static kp_status by_layout(const GemmProblem& g, int stages, cudaStream_t s) {
     // A normal = K-major, A transposed = MN-major; B transposed = K-major, B normal = MN-major
@@ -536,6 +864,7 @@ kp_status launch(kp_family fam, const kp_config& c, const GemmProblem& g, cudaSt
     if (!al(g.A, g.lda, g.sa) || !al(g.B, g.ldb, g.sb))
         return fail(KP_ERR_ALIGNMENT,
                     "tcgen05 families need 16-byte aligned operands and row/batch pitches");
+    if (c.row_tile == 2) return fam == KP_BF16_TC ? by_tile_pair<2>(c, g, s) : by_tile_pair<4>(c, g, s);
     const bool persistent = c.wg_rows == 16;
     if (fam == KP_BF16_TC) return persistent ? by_tile<2, 2>(c, g, s) : by_tile<2, 1>(c, g, s);
     return persistent ? by_tile<4, 2>(c, g, s) : by_tile<4, 1>(c, g, s);

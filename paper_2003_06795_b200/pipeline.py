@@ -23,6 +23,8 @@ import sys
 import tempfile
 from pathlib import Path
 
+import numpy as np
+
 from . import dataset, libgen, pruning, report, selector_models
 
 ROOT = Path(__file__).resolve().parent.parent
@@ -61,10 +63,42 @@ def choose(split: dataset.DataSplit, methods, budgets, seed: int):
     return rows
 
 
+def cross_validate(train: dataset.PerformanceMatrix, methods, budgets, seed: int,
+                   folds: int = 5) -> list[dict]:
+    """k-fold CV of (pruning method, budget) -> decision-tree selector score,
+    on the TRAINING side only (the held-out split is never consulted). Folds
+    come from the reference's seeded shuffle (dataset.split on the train
+    matrix with a per-fold seed)."""
+    rows = []
+    for method in methods:
+        for budget in budgets:
+            scores = []
+            for f in range(folds):
+                part = dataset.split(train, 1.0 / folds, seed * 1000 + f)
+                opts = report.default_prune_options(part.train)
+                sel = pruning.prune(method, part.train, budget, seed, opts)
+                model = selector_models.train_model(
+                    "decision-tree", selector_models.make_labels(part.train, sel), seed)
+                scores.append(selector_models.evaluate_model(model, part.test)
+                              .geomean_relative_performance)
+            rows.append({"method": method, "budget": budget,
+                         "cv_geomean": float(np.exp(np.mean(np.log(scores))))})
+    return rows
+
+
 def build_selector(data, family: str, trans: str, method: str, budget: int, seed: int = 42,
                    test_fraction: float = 0.2, out_dir: Path | None = None) -> dict:
+    """Prune + train + report. method == "auto": pick (method, budget <= the
+    given budget) by 5-fold cross-validation on the training split."""
     matrix = load_matrix(data)
     split = dataset.split(matrix, test_fraction, seed)
+    cv = None
+    if method == "auto":
+        budgets = tuple(b for b in (4, 6, 8) if b <= budget) or (budget,)
+        cv = cross_validate(split.train, ("top-count", "kmeans", "pca-kmeans", "decision-tree"),
+                            budgets, seed)
+        best = max(cv, key=lambda r: (r["cv_geomean"], -r["budget"]))
+        method, budget = best["method"], best["budget"]
     opts = report.default_prune_options(split.train)
     sel = pruning.prune(method, split.train, budget, seed, opts)
     model = selector_models.train_model(
@@ -82,6 +116,8 @@ def build_selector(data, family: str, trans: str, method: str, budget: int, seed
         "decision_tree_pct": selector_models.evaluate_model(model, split.test).percent,
         "train_decision_tree_pct": selector_models.evaluate_model(model, split.train).percent,
     }
+    if cv is not None:
+        summary["cross_validation"] = cv
     (out_dir / "summary.json").write_text(json.dumps(summary, indent=2) + "\n")
     return summary
 
@@ -91,7 +127,8 @@ def main(argv=None) -> int:
     ap.add_argument("--data", required=True)
     ap.add_argument("--family", default="f32", choices=tuple(libgen.FAMILY_IDS))
     ap.add_argument("--trans", default="nn", choices=libgen.TRANS)
-    ap.add_argument("--method", default="pca-kmeans", choices=pruning.METHODS)
+    ap.add_argument("--method", default="auto", choices=pruning.METHODS + ("auto",),
+                    help="pruning method; auto = 5-fold CV on the training split")
     ap.add_argument("--budget", type=int, default=8)
     ap.add_argument("--seed", type=int, default=42)
     ap.add_argument("--survey", action="store_true", help="also score every method x budget")

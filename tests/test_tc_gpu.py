@@ -49,7 +49,7 @@ def _check(family, cfg, m, k, n, ta, tb, batch=1, seed=0):
 @pytest.mark.parametrize("family", ["bf16", "tf32"])
 def test_family_configs_enumerate(family):
     cfgs = _gemm().family_configs(family)
-    assert len(cfgs) == 32
+    assert len(cfgs) == 40
     assert list(cfgs) == sorted(cfgs)
 
 
@@ -63,7 +63,7 @@ def test_all_configs_layouts(family, ta, tb):
 @pytest.mark.parametrize("family", ["bf16", "tf32"])
 @pytest.mark.parametrize("shape", [(1, 8, 8), (128, 64, 256), (257, 520, 136), (1024, 1024, 1024)])
 def test_shapes(family, shape):
-    for cfg in [(1, 1, 1, 8, 8), (4, 1, 4, 8, 8), (8, 1, 8, 8, 8)]:
+    for cfg in [(1, 1, 1, 8, 8), (4, 1, 4, 8, 8), (8, 1, 8, 8, 8), (4, 1, 8, 16, 16), (4, 2, 8, 16, 16)]:
         _check(family, cfg, *shape, ta=False, tb=False, seed=7)
 
 

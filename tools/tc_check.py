@@ -33,6 +33,5 @@ if __name__ == "__main__":
     fams = sys.argv[1].split(",") if len(sys.argv) > 1 else ["tf32", "bf16"]
     for fam in fams:
         for trans in ("tn", "nn", "nt", "tt"):
-            for cfg in [(1, 1, 1, 8, 8), (1, 1, 8, 8, 8)]:
-                if not check(fam, cfg, 256, 256, 256, trans) and "ERROR" in "":
-                    pass
+            for cfg in [(1, 1, 1, 8, 8), (4, 1, 8, 16, 16), (4, 2, 4, 16, 16), (4, 2, 8, 16, 16)]:
+                check(fam, cfg, 520, 264, 776, trans)
