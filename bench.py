@@ -238,9 +238,9 @@ class FamilyRun:
 
     def barrier(self):
         import torch.distributed as dist
-        if self.world > 1:
-            dist.barrier()
         self.torch.cuda.synchronize()
+        if self.world > 1:
+            dist.barrier(group=self.gloo)
 
     def sweep(self):
         import torch.distributed as dist
@@ -313,13 +313,15 @@ class FamilyRun:
         return per_size, pct, dom, mean_ms
 
 
-def max_over_ranks(x, world, dev):
+def reduce_over_ranks(x, world, group, op="max"):
+    """Host-side reduction of a device-timed scalar (gloo group): the max over
+    ranks for times, the sum for launch counts."""
     if world == 1:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], device=dev, dtype=torch.float64)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t = torch.tensor([float(x)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM, group=group)
     return float(t.item())
 
 
@@ -335,12 +337,20 @@ def run_gpu(args) -> int:
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # KP_BENCH_SHARE_DEVICE=1 runs every rank on device 0 with a gloo-only
+    # process group: exercises the multi-rank code path on a one-GPU box
+    share = os.environ.get("KP_BENCH_SHARE_DEVICE") == "1"
+    dev_index = 0 if share else local
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
     gloo = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-        gloo = dist.new_group(backend="gloo")
+        if share:
+            dist.init_process_group("gloo")
+            gloo = dist.group.WORLD
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+            gloo = dist.new_group(backend="gloo")
     step_flops = sum(flops_of(s) for s in SIZES)
 
     # ---- headline family: FP32 SIMT (the paper's 640-config space) ---------
@@ -351,11 +361,8 @@ def run_gpu(args) -> int:
     clocks = ClockSampler()
     per_size_ms, launches = f32.timed(args.steps, clocks)
     clk = clocks.stop(gpu_index())
-    total_ms = max_over_ranks(float(per_size_ms.sum()), world, dev)
-    if world > 1:
-        lt = torch.tensor([launches], device=dev, dtype=torch.int64)
-        dist.all_reduce(lt)
-        launches = int(lt.item())
+    total_ms = reduce_over_ranks(float(per_size_ms.sum()), world, gloo)
+    launches = int(reduce_over_ranks(launches, world, gloo, op="sum"))
     value = world * args.steps * step_flops / (total_ms * 1e-3) / 1e12
 
     # ---- e2e through the host-buffer API --------------------------------
@@ -369,7 +376,7 @@ def run_gpu(args) -> int:
     for _ in range(args.steps):
         for ha, hb, hc in host:
             gemm.matmul_pinned(ha, hb, hc)
-    e2e_s = max_over_ranks(time.perf_counter() - t0, world, dev)
+    e2e_s = reduce_over_ranks(time.perf_counter() - t0, world, gloo)
     e2e_value = world * args.steps * step_flops / e2e_s / 1e12
 
     # ---- tensor-core families (same workload, their own selectors) -------
@@ -379,7 +386,7 @@ def run_gpu(args) -> int:
         run = FamilyRun(fam, args, dev, rank, world, gloo)
         run.sweep()
         ms, _ = run.timed(fam_steps)
-        tot = max_over_ranks(float(ms.sum()), world, dev)
+        tot = reduce_over_ranks(float(ms.sum()), world, gloo)
         per, pct, dom, mean = run.report(ms)
         tpk, src = tensor_peak(fam)
         ach = flops_of(SIZES[dom]) / (mean[dom] * 1e-3) / 1e12

@@ -80,3 +80,26 @@ def test_sweep_records_canonical_order():
     assert [r.config for r in recs] == list(cfgs) * 2
     assert recs[0].gflops == pytest.approx(2 * 2 * 3 * 4 / 10.0)
     assert recs[0].runtime_ns == pytest.approx(10.0)
+
+
+def _reduce_worker(rank, world, port, out):
+    import sys
+    import torch.distributed as dist
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    import bench
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    out[rank] = (bench.reduce_over_ranks(1.5 + rank, world, dist.group.WORLD),
+                 bench.reduce_over_ranks(10 * (rank + 1), world, dist.group.WORLD, op="sum"))
+    dist.destroy_process_group()
+
+
+def test_bench_reductions_world2():
+    """bench.py times every rank on its device and reports the max over ranks
+    (launch counts summed); the reduction runs on the host gloo group."""
+    port = _free_port()
+    manager = mp.Manager()
+    out = manager.dict()
+    mp.spawn(_reduce_worker, args=(2, port, out), nprocs=2, join=True)
+    assert out[0] == out[1] == (2.5, 30.0)
