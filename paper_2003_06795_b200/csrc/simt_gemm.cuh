@@ -230,7 +230,10 @@ __device__ __forceinline__ float epilogue(float acc, float alpha, float beta, co
 }
 
 template <int ACC, int RT, int CT, bool TA, bool TB, int BK>
-__global__ void __launch_bounds__(256, 2) simt_gemm_kernel(const Params p) {
+#ifndef KP_SIMT_MIN_BLOCKS
+#define KP_SIMT_MIN_BLOCKS 2
+#endif
+__global__ void __launch_bounds__(256, KP_SIMT_MIN_BLOCKS) simt_gemm_kernel(const Params p) {
     constexpr int LOG_BK = Geo<BK>::LOG_BK;
     extern __shared__ __align__(16) float smem[];
     const int tid = threadIdx.x;

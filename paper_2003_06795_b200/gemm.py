@@ -23,8 +23,6 @@ import numpy as np
 from . import _native as nat
 from .dataset import KernelConfig
 
-_DTYPE_OF = {}
-
 
 def _torch():
     import torch

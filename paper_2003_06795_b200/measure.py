@@ -18,7 +18,6 @@ parent and are merged back into canonical order.
 from __future__ import annotations
 
 import json
-import math
 import os
 import time
 from dataclasses import dataclass, field
@@ -289,10 +288,6 @@ def sidecar(result: SweepResult, extra: dict | None = None) -> dict:
     return doc
 
 
-def square_problems(sizes=(64, 128, 256, 512, 1024, 2048)) -> tuple[ProblemSize, ...]:
-    return tuple(ProblemSize(s, s, s) for s in sizes)
-
-
 def main(argv=None) -> int:
     import argparse
     ap = argparse.ArgumentParser(description="measured config x size sweep (one GPU)")
@@ -303,6 +298,7 @@ def main(argv=None) -> int:
     ap.add_argument("--top", type=int, default=5)
     ap.add_argument("--out")
     args = ap.parse_args(argv)
+    from .shapes import square_problems
     probs = square_problems(tuple(int(s) for s in args.sizes.split(",")))
     spec = SweepSpec(probs, family=args.family, reps=args.reps, warmup=args.warmup)
 

@@ -152,3 +152,41 @@ def test_timing_loop_positive():
     assert ns > 0.0
     res = _gemm().sweep_problem(a, a, ds.all_configs()[:10], reps=3)
     assert len(res) == 10 and all(v > 0 for v in res)
+
+
+def test_runtime_selection_full_and_lean_library():
+    """kp_gemm_auto through the compiled selector: bit-exact vs the oracle in
+    the full library and in libkp_lean.so (only selector-reachable kernels),
+    and both libraries choose the same config."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    lean = root / "paper_2003_06795_b200" / "libkp_lean.so"
+    if not lean.exists():
+        pytest.skip("lean library not built")
+    script = r'''
+import json, sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from paper_2003_06795_b200 import gemm
+from oracle.gemm_oracle import gemm_f32_exact
+out = []
+for (m, k, n) in [(17, 27, 15), (200, 576, 64), (1, 4096, 1000), (512, 512, 512)]:
+    rng = np.random.default_rng(m + k + n)
+    a = rng.uniform(-1, 1, (m, k)).astype(np.float32)
+    b = rng.uniform(-1, 1, (k, n)).astype(np.float32)
+    c = gemm.matmul(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()).cpu().numpy()
+    ok = bool(np.array_equal(c, gemm_f32_exact(a, b, m=m, k=k, n=n).reshape(m, n)))
+    out.append([m, k, n, list(gemm.select(m, k, n).as_tuple()), ok])
+print(json.dumps(out))
+'''
+    res = {}
+    for name, path in (("full", root / "paper_2003_06795_b200" / "libkp.so"), ("lean", lean)):
+        env = dict(__import__("os").environ, KP_LIB_PATH=str(path))
+        run = subprocess.run([sys.executable, "-c", script, str(root)], env=env,
+                             capture_output=True, text=True, timeout=300)
+        assert run.returncode == 0, run.stderr[-2000:]
+        res[name] = json.loads(run.stdout.strip().splitlines()[-1])
+    assert res["full"] == res["lean"]
+    assert all(row[-1] for row in res["full"])
