@@ -156,6 +156,61 @@ def matmul_pinned(a_host, b_host, out_host, config=None, *, family="f32"):
     return out_host
 
 
+class PinnedPipeline:
+    """End-to-end GEMMs on pinned host buffers with the copies overlapped:
+    H2D of problem i+1 (copy-in stream) runs under the kernel of problem i
+    (compute stream) and the D2H of problem i-1 (copy-out stream); events
+    order the three streams. Device buffers are cached per shape."""
+
+    def __init__(self, family="f32"):
+        torch = _torch()
+        self.family = family
+        self.want = _family_dtype(nat.family_id(family))
+        self.dev = torch.device("cuda", torch.cuda.current_device())
+        self.s_in = torch.cuda.Stream(self.dev)
+        self.s_run = torch.cuda.Stream(self.dev)
+        self.s_out = torch.cuda.Stream(self.dev)
+        self._bufs = {}
+
+    def _buffers(self, i, a_host, b_host, out_host):
+        torch = _torch()
+        key = (i, tuple(a_host.shape), tuple(b_host.shape))
+        if key not in self._bufs:
+            self._bufs[key] = (torch.empty(a_host.shape, dtype=a_host.dtype, device=self.dev),
+                               torch.empty(b_host.shape, dtype=b_host.dtype, device=self.dev),
+                               torch.empty(out_host.shape, dtype=torch.float32, device=self.dev))
+        return self._bufs[key]
+
+    def run(self, problems, configs=None):
+        """problems: [(a_host, b_host, out_host)] pinned; returns when all
+        results are in the host buffers."""
+        torch = _torch()
+        done_in, done_run = [], []
+        for i, (ha, hb, hc) in enumerate(problems):
+            da, db, dc = self._buffers(i, ha, hb, hc)
+            with torch.cuda.stream(self.s_in):
+                da.copy_(ha, non_blocking=True)
+                db.copy_(hb, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(self.s_in)
+                done_in.append(ev)
+        for i, (ha, hb, hc) in enumerate(problems):
+            da, db, dc = self._buffers(i, ha, hb, hc)
+            with torch.cuda.stream(self.s_run):
+                self.s_run.wait_event(done_in[i])
+                xa, xb = (da, db) if da.dtype == self.want else (da.to(self.want), db.to(self.want))
+                matmul(xa, xb, None if configs is None else configs[i], family=self.family,
+                       out=dc)
+                ev = torch.cuda.Event()
+                ev.record(self.s_run)
+                done_run.append(ev)
+            with torch.cuda.stream(self.s_out):
+                self.s_out.wait_event(ev)
+                hc.copy_(dc, non_blocking=True)
+        self.s_out.synchronize()
+        return [hc for _, _, hc in problems]
+
+
 def time_config(a, b, config, *, family="f32", out=None, warmup: int = 3, reps: int = 10,
                 min_sample_ns: float = 50_000.0, max_cell_ns: float = 0.0) -> float:
     """Median per-launch device time (ns) of one config on one problem."""
