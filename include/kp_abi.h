@@ -125,6 +125,22 @@ kp_status kp_gemm_auto(kp_family family, const kp_gemm_desc* desc,
                        const void* A, const void* B, float* C, void* stream,
                        kp_config* chosen /* may be NULL */);
 
+/* ---- im2col front-end (network layers as the selectors' GEMMs) -------- */
+/* NCHW input, weights [c_out, c_in*kh*kw] row-major, output NHWC
+ * [batch*ho*wo, c_out]; the GEMM is the NT variant (kp_gemm_auto with
+ * trans_b = 1), so conv layers run through the compiled NT selector.
+ * Tensor-core families additionally need 16-byte aligned K pitches. */
+typedef struct {
+    int64_t batch, c_in, h, w, c_out, kh, kw, stride_h, stride_w, pad_h, pad_w;
+} kp_conv_desc;
+kp_status kp_conv_output_shape(const kp_conv_desc* d, int64_t* ho, int64_t* wo);
+/* cols[batch*ho*wo, c_in*kh*kw] (fp32, bf16 for KP_BF16_TC), zero padding. */
+kp_status kp_im2col(kp_family family, const kp_conv_desc* d, const void* x, void* cols,
+                    void* stream);
+kp_status kp_conv2d_auto(kp_family family, const kp_conv_desc* d, const void* x,
+                         const void* w, float* y, void* cols /* workspace */, void* stream,
+                         kp_config* chosen /* may be NULL */);
+
 /* ---- diagnostics -------------------------------------------------------- */
 const char* kp_status_string(kp_status status);
 const char* kp_last_error(void);               /* thread-local */

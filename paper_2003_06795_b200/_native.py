@@ -31,7 +31,7 @@ KP_ERR_INVALID_ARG = 6
 EXPORTS = ("kp_abi_version", "kp_num_configs", "kp_config_at", "kp_config_valid",
            "kp_gemm", "kp_gemm_time", "kp_sweep_problem", "kp_select", "kp_gemm_auto",
            "kp_status_string", "kp_last_error", "kp_launch_count", "kp_device_info",
-           "kp_fp32_peak")
+           "kp_fp32_peak", "kp_conv_output_shape", "kp_im2col", "kp_conv2d_auto")
 
 
 class KpConfig(ctypes.Structure):
@@ -49,6 +49,11 @@ class KpGemmDesc(ctypes.Structure):
                 ("lda", ctypes.c_int64), ("ldb", ctypes.c_int64), ("ldc", ctypes.c_int64),
                 ("stride_a", ctypes.c_int64), ("stride_b", ctypes.c_int64),
                 ("stride_c", ctypes.c_int64), ("alpha", ctypes.c_float), ("beta", ctypes.c_float)]
+
+
+class KpConvDesc(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_int64) for f in ("batch", "c_in", "h", "w", "c_out", "kh", "kw",
+                                              "stride_h", "stride_w", "pad_h", "pad_w")]
 
 
 class KernelLibraryError(RuntimeError):
@@ -97,6 +102,10 @@ def _declare(lib):
         "kp_launch_count": (c.c_int64, []),
         "kp_device_info": (c.c_int, [c.c_int32, P(c.c_int32), P(c.c_int32), P(c.c_int32)]),
         "kp_fp32_peak": (c.c_int, [P(c.c_double), c.c_void_p]),
+        "kp_conv_output_shape": (c.c_int, [P(KpConvDesc), P(c.c_int64), P(c.c_int64)]),
+        "kp_im2col": (c.c_int, [c.c_int, P(KpConvDesc), c.c_void_p, c.c_void_p, c.c_void_p]),
+        "kp_conv2d_auto": (c.c_int, [c.c_int, P(KpConvDesc), c.c_void_p, c.c_void_p, c.c_void_p,
+                                     c.c_void_p, c.c_void_p, P(KpConfig)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
