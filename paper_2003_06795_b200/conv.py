@@ -41,6 +41,8 @@ def im2col(x, kh: int, kw: int, stride=1, padding=0, family="f32"):
     """cols [B*Ho*Wo, Cin*kh*kw] of an NCHW CUDA tensor (zero padding)."""
     torch = _torch()
     fam = nat.family_id(family)
+    if x.dtype != _family_dtype(fam):
+        raise nat.BadProblemShape(f"family {family!r} expects {_family_dtype(fam)} input")
     w_shape = (1, x.shape[1], kh, kw)
     ho, wo = output_shape(x.shape, w_shape, stride, padding)
     x = x.contiguous()

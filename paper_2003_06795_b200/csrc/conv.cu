@@ -4,9 +4,8 @@
 //   K = Cin*kh*kw (col = c*kh*kw + r*kw + s), zero for padded taps;
 //   y[M, Cout] (NHWC) = cols @ W^T, W stored [Cout, K] row-major -> the GEMM
 //   is the NT variant (trans_b), dispatched through the compiled selector.
-// The gather is HBM/L2-bound integer work: one thread per cols element,
-// consecutive threads along K (coalesced 4-byte stores), grid-stride loop
-// sized to a multiple of the SM count.
+// The gather is HBM-bound byte movement (the cols write dominates; see the
+// tiled kernel below), not GEMM-shaped work.
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -15,28 +14,126 @@
 
 namespace kp {
 
-template <typename T>
-__global__ void __launch_bounds__(256) im2col_kernel(const T* __restrict__ x, T* __restrict__ cols,
-                                                     kp_conv_desc d, int64_t ho, int64_t wo,
-                                                     int64_t total) {
-    const int64_t K = d.c_in * d.kh * d.kw;
-    const int64_t khw = d.kh * d.kw;
-    for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
-         idx += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t row = idx / K, col = idx - row * K;
-        const int64_t b = row / (ho * wo);
-        const int64_t pix = row - b * ho * wo;
-        const int64_t oh = pix / wo, ow = pix - oh * wo;
-        const int64_t c = col / khw;
-        const int64_t rs = col - c * khw;
-        const int64_t r = rs / d.kw, s = rs - r * d.kw;
-        const int64_t ih = oh * d.stride_h - d.pad_h + r;
-        const int64_t iw = ow * d.stride_w - d.pad_w + s;
-        T v = T(0.0f);
-        if (ih >= 0 && ih < d.h && iw >= 0 && iw < d.w)
-            v = x[((b * d.c_in + c) * d.h + ih) * d.w + iw];
-        cols[idx] = v;
+// Unsigned 32-bit division by a run-time constant as a multiply-high + shift
+// (valid for dividends < 2^31): the gather's index decomposition would
+// otherwise be dominated by integer divides.
+struct FastDiv {
+    uint32_t d, magic, shift;
+    FastDiv() = default;
+    explicit FastDiv(uint32_t div) : d(div) {
+        shift = 0;
+        while ((1ull << shift) < div) ++shift;
+        magic = uint32_t(((1ull << 32) * ((1ull << shift) - div)) / div + 1);
     }
+    __device__ __forceinline__ uint32_t div(uint32_t n) const {
+        return (__umulhi(n, magic) + n) >> shift;
+    }
+};
+
+struct Im2colGeom {
+    FastDiv hwo, wo, khw, kw;
+    int32_t c_in, h, w, kh, stride_h, stride_w, pad_h, pad_w;
+};
+
+// Tiled gather: a CTA owns 64 consecutive output pixels (cols rows) and walks
+// K in chunks of 64 taps.  Gather phase: lanes run along pixels, so for every
+// tap (c, r, s) a warp reads consecutive input columns (coalesced for stride
+// 1; neighbouring pixels' receptive fields overlap, so most re-reads hit
+// L1/L2), 16 independent loads in flight per thread; the chunk's tap table is
+// decoded once into shared memory.  Write phase: the tile is read back
+// transposed (padded rows, <= 2-way conflicts) and stored as 16-byte vectors
+// along K (VEC: K a multiple of 16/sizeof(T) and a 16-byte aligned cols),
+// otherwise as coalesced scalars.  Both HBM streams are coalesced; the kernel
+// is bound by the cols write (x is re-read from L2).
+constexpr int kIm2colPix = 64;
+constexpr int kIm2colKC = 64;
+
+template <typename T, bool VEC>
+__global__ void __launch_bounds__(256) im2col_tiled_kernel(const T* __restrict__ x,
+                                                           T* __restrict__ cols, Im2colGeom g,
+                                                           uint32_t rows, uint32_t K) {
+    constexpr int KC = kIm2colKC, PIX = kIm2colPix;
+    __shared__ T tile[KC][PIX + 1];
+    __shared__ int32_t tab_off[KC], tab_r[KC], tab_s[KC];
+    const int t = threadIdx.x;
+    const int p = t & (PIX - 1), grp = t >> 6;
+    const uint32_t row0 = blockIdx.x * PIX;
+    const uint32_t prow = row0 + p;
+    const bool pvalid = prow < rows;
+    const uint32_t b = g.hwo.div(prow);
+    const uint32_t pix = prow - b * g.hwo.d;
+    const uint32_t oh = g.wo.div(pix), ow = pix - oh * g.wo.d;
+    const int32_t ih0 = int32_t(oh) * g.stride_h - g.pad_h;
+    const int32_t iw0 = int32_t(ow) * g.stride_w - g.pad_w;
+    const T* xp = x + int64_t(b) * g.c_in * g.h * g.w + int64_t(ih0) * g.w + iw0;
+    for (uint32_t k0 = blockIdx.y * KC; k0 < K; k0 += gridDim.y * KC) {
+        if (t < KC && k0 + t < K) {
+            const uint32_t k = k0 + t;
+            const uint32_t c = g.khw.div(k);
+            const uint32_t rs = k - c * g.khw.d;
+            const uint32_t r = g.kw.div(rs);
+            const uint32_t sc = rs - r * g.kw.d;
+            tab_off[t] = int32_t((c * g.h + r) * g.w + sc);
+            tab_r[t] = int32_t(r);
+            tab_s[t] = int32_t(sc);
+        }
+        __syncthreads();
+        // Branch-free gather: every lane issues all KC/4 loads back to back
+        // (out-of-range taps read a valid dummy address and are zeroed
+        // after), so their latencies overlap instead of serialising behind
+        // per-tap branches.
+        T v[KC / 4];
+        bool in[KC / 4];
+#pragma unroll
+        for (int i = 0; i < KC / 4; ++i) {
+            const int j = grp + 4 * i;
+            const int32_t ih = ih0 + tab_r[j], iw = iw0 + tab_s[j];
+            in[i] = pvalid && k0 + j < K && unsigned(ih) < unsigned(g.h) &&
+                    unsigned(iw) < unsigned(g.w);
+            v[i] = __ldg(in[i] ? xp + tab_off[j] : x);
+        }
+#pragma unroll
+        for (int i = 0; i < KC / 4; ++i) tile[grp + 4 * i][p] = in[i] ? v[i] : T(0.0f);
+        __syncthreads();
+        if constexpr (VEC) {
+            constexpr int VW = 16 / int(sizeof(T));  // elements per 16-byte store
+            constexpr int LPR = KC / VW;             // threads per row segment
+            constexpr int RPP = 256 / LPR;           // rows per pass
+            const int q = t % LPR;
+            const uint32_t kk = k0 + q * VW;
+#pragma unroll
+            for (int pass = 0; pass < PIX / RPP; ++pass) {
+                const int pr = t / LPR + pass * RPP;
+                const uint32_t row = row0 + pr;
+                if (row < rows && kk < K) {
+                    union { uint4 u; T e[VW]; } out;
+#pragma unroll
+                    for (int e = 0; e < VW; ++e) out.e[e] = tile[q * VW + e][pr];
+                    *reinterpret_cast<uint4*>(cols + int64_t(row) * K + kk) = out.u;
+                }
+            }
+        } else {
+#pragma unroll 4
+            for (int idx = t; idx < PIX * KC; idx += 256) {
+                const int pr = idx / KC, j = idx % KC;
+                const uint32_t row = row0 + pr;
+                if (row < rows && k0 + j < K) cols[int64_t(row) * K + k0 + j] = tile[j][pr];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+template <typename T, bool VEC>
+static void launch_im2col_tiled(const T* x, T* cols, const Im2colGeom& g, int64_t rows,
+                                int64_t K, int sms, cudaStream_t s) {
+    const int64_t gx = (rows + kIm2colPix - 1) / kIm2colPix;
+    const int64_t kchunks = (K + kIm2colKC - 1) / kIm2colKC;
+    const int64_t gy = std::min<int64_t>(
+        std::min<int64_t>(kchunks, 65535), std::max<int64_t>(1, (int64_t(sms) * 8 + gx - 1) / gx));
+    im2col_tiled_kernel<T, VEC><<<dim3(unsigned(gx), unsigned(gy)), 256, 0, s>>>(
+        x, cols, g, uint32_t(rows), uint32_t(K));
+    note_launch();
 }
 
 static kp_status conv_shape(const kp_conv_desc* d, int64_t* ho, int64_t* wo) {
@@ -65,20 +162,43 @@ extern "C" kp_status kp_im2col(kp_family family, const kp_conv_desc* d, const vo
     kp_status st = conv_shape(d, &ho, &wo);
     if (st != KP_OK) return st;
     if (!x || !cols) return fail(KP_ERR_INVALID_ARG, "null tensor");
-    const int64_t total = d->batch * ho * wo * d->c_in * d->kh * d->kw;
+    const int64_t K = d->c_in * d->kh * d->kw, hwo = ho * wo;
+    if (K >= (1ll << 30) || hwo >= (1ll << 30) || d->c_in * d->h * d->w >= (1ll << 31))
+        return fail(KP_ERR_BAD_SHAPE, "conv dims exceed the 2^31 gather range");
+    const bool bf16 = family == KP_BF16_TC;
+    const int esz = bf16 ? 2 : 4;
+    const bool vec = K % (16 / esz) == 0 && aligned16(cols);
+    Im2colGeom g;
+    g.hwo = FastDiv(uint32_t(hwo));
+    g.wo = FastDiv(uint32_t(wo));
+    g.khw = FastDiv(uint32_t(d->kh * d->kw));
+    g.kw = FastDiv(uint32_t(d->kw));
+    g.c_in = int32_t(d->c_in); g.h = int32_t(d->h); g.w = int32_t(d->w); g.kh = int32_t(d->kh);
+    g.stride_h = int32_t(d->stride_h); g.stride_w = int32_t(d->stride_w);
+    g.pad_h = int32_t(d->pad_h); g.pad_w = int32_t(d->pad_w);
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t blocks = std::min<int64_t>((total + 255) / 256, int64_t(sms) * 16);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (family == KP_BF16_TC)
-        im2col_kernel<__nv_bfloat16><<<unsigned(blocks), 256, 0, s>>>(
-            static_cast<const __nv_bfloat16*>(x), static_cast<__nv_bfloat16*>(cols), *d, ho, wo, total);
-    else
-        im2col_kernel<float><<<unsigned(blocks), 256, 0, s>>>(
-            static_cast<const float*>(x), static_cast<float*>(cols), *d, ho, wo, total);
-    note_launch();
-    return check_launch("im2col_kernel");
+    // Rows per launch stay below 2^31 (FastDiv's range): split over images.
+    const int64_t imgs = std::max<int64_t>(1, ((1ll << 31) - 2 * kIm2colPix) / hwo);
+    for (int64_t b0 = 0; b0 < d->batch; b0 += imgs) {
+        const int64_t nb = std::min(imgs, d->batch - b0);
+        const int64_t xoff = b0 * d->c_in * d->h * d->w, coff = b0 * hwo * K;
+        if (bf16) {
+            auto xp = static_cast<const __nv_bfloat16*>(x) + xoff;
+            auto cp = static_cast<__nv_bfloat16*>(cols) + coff;
+            if (vec) launch_im2col_tiled<__nv_bfloat16, true>(xp, cp, g, nb * hwo, K, sms, s);
+            else launch_im2col_tiled<__nv_bfloat16, false>(xp, cp, g, nb * hwo, K, sms, s);
+        } else {
+            auto xp = static_cast<const float*>(x) + xoff;
+            auto cp = static_cast<float*>(cols) + coff;
+            if (vec) launch_im2col_tiled<float, true>(xp, cp, g, nb * hwo, K, sms, s);
+            else launch_im2col_tiled<float, false>(xp, cp, g, nb * hwo, K, sms, s);
+        }
+        if ((st = check_launch("im2col_kernel")) != KP_OK) return st;
+    }
+    return KP_OK;
 }
 
 extern "C" kp_status kp_conv2d_auto(kp_family family, const kp_conv_desc* d, const void* x,

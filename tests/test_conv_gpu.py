@@ -48,20 +48,32 @@ def test_conv2d_f32_bit_exact(case):
     np.testing.assert_allclose(got.transpose(0, 3, 1, 2), ref, rtol=1e-4, atol=1e-5)
 
 
-def test_im2col_matches_numpy():
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("shape", [
+    (2, 5, 9, 11, 3, 2, 2, 1),      # K = 30: scalar gather
+    (2, 8, 33, 31, 3, 3, 1, 1),     # K = 72: 16-byte vector stores (both dtypes)
+    (3, 4, 64, 64, 1, 1, 1, 0),     # K = 4: f32 vectors, bf16 scalar
+    (1, 3, 50, 50, 7, 7, 2, 3),     # stem-like, K = 147
+])
+def test_im2col_matches_numpy(shape, dtype):
     from paper_2003_06795_b200 import conv
+    b, c, h, w, kh, kw, st, pad = shape
     rng = np.random.default_rng(1)
-    x = rng.uniform(-1, 1, (2, 5, 9, 11)).astype(np.float32)
-    got = conv.im2col(torch.from_numpy(x).cuda(), 3, 2, stride=2, padding=1).cpu().numpy()
-    b, c, h, w = x.shape
-    xp = np.zeros((b, c, h + 2, w + 2), dtype=np.float32)
-    xp[:, :, 1:1 + h, 1:1 + w] = x
-    ho, wo = (h + 2 - 3) // 2 + 1, (w + 2 - 2) // 2 + 1
-    want = np.empty((b, ho, wo, c, 3, 2), dtype=np.float32)
-    for r in range(3):
-        for s in range(2):
-            want[..., r, s] = xp[:, :, r:r + 2 * ho:2, s:s + 2 * wo:2].transpose(0, 2, 3, 1)
-    np.testing.assert_array_equal(got, want.reshape(b * ho * wo, c * 6))
+    x = rng.uniform(-1, 1, (b, c, h, w)).astype(np.float32)
+    xt = torch.from_numpy(x).cuda()
+    if dtype == "bf16":
+        xt = xt.to(torch.bfloat16)
+        x = xt.float().cpu().numpy()
+    got = conv.im2col(xt, kh, kw, stride=st, padding=pad,
+                      family=dtype).float().cpu().numpy()
+    xp = np.zeros((b, c, h + 2 * pad, w + 2 * pad), dtype=np.float32)
+    xp[:, :, pad:pad + h, pad:pad + w] = x
+    ho, wo = (h + 2 * pad - kh) // st + 1, (w + 2 * pad - kw) // st + 1
+    want = np.empty((b, ho, wo, c, kh, kw), dtype=np.float32)
+    for r in range(kh):
+        for s in range(kw):
+            want[..., r, s] = xp[:, :, r:r + st * ho:st, s:s + st * wo:st].transpose(0, 2, 3, 1)
+    np.testing.assert_array_equal(got, want.reshape(b * ho * wo, c * kh * kw))
 
 
 @pytest.mark.parametrize("family", ["tf32", "bf16"])

@@ -76,8 +76,11 @@ def main() -> int:
                 ws = torch.empty(args.batch * ho * ho * kk, dtype=dt, device="cuda")
                 ms = time_ms(lambda: conv.conv2d(x, w, st, pad, family=fam, nhwc=True,
                                                  workspace=ws))
+                im_ms = time_ms(lambda: conv.im2col(x, k, k, st, pad, family=fam))
                 cfg = gemm.select(args.batch * ho * ho, kk, cout, family=fam, trans_b=True)
                 row[fam] = {"ms": ms, "tflops": flops / (ms * 1e-3) / 1e12,
+                            "im2col_ms": im_ms,
+                            "im2col_gbs": (x.numel() + ws.numel()) * x.element_size() / im_ms / 1e6,
                             "config": list(cfg.as_tuple())}
             ref = time_ms(lambda: torch.nn.functional.conv2d(x32, w32, stride=st, padding=pad))
             row["cudnn_fp32_ms"] = ref
