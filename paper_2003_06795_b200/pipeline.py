@@ -43,7 +43,7 @@ def materialize(path) -> Path:
 
 
 def load_matrix(path) -> dataset.PerformanceMatrix:
-    return dataset.normalize(dataset.build_matrix(dataset.load_records(materialize(path))))
+    return dataset.normalize(dataset.load_matrix(materialize(path)))
 
 
 def choose(split: dataset.DataSplit, methods, budgets, seed: int):
