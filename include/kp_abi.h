@@ -31,7 +31,8 @@
  *
  * Conventions: every entry point returns a status and never aborts; the
  * library allocates no device memory per call (TMEM is allocated/freed inside
- * the tcgen05 kernels); calls are stream-ordered and reentrant; the message of
+ * the tcgen05 kernels; a 256 KB ring of stream-K hand-off flags is allocated
+ * once per device on first use); calls are stream-ordered and reentrant; the message of
  * the last failure on the calling thread is available from kp_last_error().
  */
 #ifndef KP_ABI_H
@@ -116,6 +117,15 @@ kp_status kp_sweep_problem(kp_family family, const kp_config* cfgs, int32_t n_cf
                            double min_sample_ns, double max_cell_ns,
                            double* runtime_ns, void* stream);
 
+/* K1 (FP32 SIMT) tile scheduling.  0 = one output tile per CTA; 1 (default)
+ * = ordered stream-K when whole tiles would leave part of the last wave idle:
+ * one persistent wave shares the (tile, k-slice) units evenly, a tile split
+ * between two CTAs is handed off through C with its k order preserved, so
+ * results stay bit-identical to mode 0 (beta == 0 problems only); 2 = ordered
+ * stream-K whenever a problem has two or more tiles (tests).  Process-wide;
+ * returns the previous mode, or -1 for an unknown mode (left unchanged). */
+int32_t   kp_set_schedule(int32_t mode);
+
 /* ---- runtime selection (generated decision-tree header) --------------- */
 /* Config the compiled selector picks for (m,k,n); KP_ERR_UNSUPPORTED when no
  * selector is compiled in for this family / transpose variant. */
@@ -150,8 +160,9 @@ int64_t     kp_launch_count(void);
  * compute capability (major*10+minor). */
 kp_status   kp_device_info(int32_t device, int32_t* sm_count, int32_t* sm_clock_khz,
                            int32_t* cc);
-/* Measured FP32 FFMA throughput of the current device (TFLOP/s, best of 5
- * full-chip launches at the clocks of the moment): the K1 roofline peak. */
+/* Measured FP32 FMA-pipe throughput of the current device (TFLOP/s, best of
+ * full-chip launches of scalar FFMA and packed FFMA2 chains at the clocks of
+ * the moment): the K1 roofline peak. */
 kp_status   kp_fp32_peak(double* tflops, void* stream);
 
 #ifdef __cplusplus

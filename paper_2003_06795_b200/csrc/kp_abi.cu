@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -31,6 +32,49 @@ kp_status check_launch(const char* what) {
     const cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) return KP_OK;
     return fail(KP_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ------------------------------------------------------- K1 scheduling --
+static std::atomic<int> g_schedule{1};
+int simt_schedule() { return g_schedule.load(std::memory_order_relaxed); }
+
+int sm_count() {
+    static int cached[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (cached[dev] == 0) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        cached[dev] = v > 0 ? v : 1;
+    }
+    return cached[dev];
+}
+
+kp_status sk_reserve(uint32_t n, SkFlags* out) {
+    static std::mutex mu;
+    static uint32_t* rings[64] = {nullptr};
+    static uint32_t next_slot[64] = {0};
+    static uint32_t next_epoch[64] = {0};
+    if (n == 0 || n > KP_SK_RING / 4) return fail(KP_ERR_UNSUPPORTED, "stream-K grid too large");
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64)
+        return fail(KP_ERR_CUDA, "stream-K: no current device");
+    std::lock_guard<std::mutex> lock(mu);
+    if (!rings[dev]) {
+        void* ptr = nullptr;
+        if (cudaMalloc(&ptr, KP_SK_RING * sizeof(uint32_t)) != cudaSuccess)
+            return check_launch("stream-K flag ring cudaMalloc");
+        if (cudaMemset(ptr, 0, KP_SK_RING * sizeof(uint32_t)) != cudaSuccess)
+            return check_launch("stream-K flag ring cudaMemset");
+        rings[dev] = static_cast<uint32_t*>(ptr);
+    }
+    if (++next_epoch[dev] == 0) ++next_epoch[dev];  // 0 is the ring's initial value
+    out->flags = rings[dev];
+    out->base = next_slot[dev];
+    out->epoch = next_epoch[dev];
+    next_slot[dev] = (next_slot[dev] + n) & KP_SK_RING_MASK;
+    return KP_OK;
 }
 
 // ---------------------------------------------------------- config space --
@@ -225,6 +269,11 @@ kp_status kp_config_at(kp_family family, int32_t index, kp_config* out) {
 }
 
 kp_status kp_config_valid(kp_family family, kp_config cfg) { return valid_config(family, cfg); }
+
+int32_t kp_set_schedule(int32_t mode) {
+    if (mode < 0 || mode > 2) return -1;
+    return g_schedule.exchange(mode);
+}
 
 kp_status kp_gemm(kp_family family, kp_config cfg, const kp_gemm_desc* desc, const void* A,
                   const void* B, float* C, void* stream) {

@@ -29,6 +29,26 @@ struct GemmProblem {
     float* C;
 };
 
+// Ordered stream-K hand-off flags: a per-device ring of KP_SK_RING u32 slots
+// (allocated and zeroed once, the only device memory the library owns).  Each
+// stream-K launch reserves gridDim.x consecutive slots and a fresh epoch, so
+// concurrent or back-to-back launches never read each other's flags.
+constexpr uint32_t KP_SK_RING = 1u << 16;
+constexpr uint32_t KP_SK_RING_MASK = KP_SK_RING - 1;
+struct SkFlags {
+    uint32_t* flags;
+    uint32_t base, epoch;
+};
+// Reserve `n` slots on the current device (KP_ERR_CUDA if the ring cannot be
+// allocated).
+kp_status sk_reserve(uint32_t n, SkFlags* out);
+// Scheduling policy of the K1 family: 0 = one tile per CTA, 1 = ordered
+// stream-K when the last wave would leave SMs idle (default), 2 = ordered
+// stream-K whenever the problem has at least two tiles (tests).
+int simt_schedule();
+// Number of SMs of the current device (cached).
+int sm_count();
+
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 // ---------------------------------------------------------------- PTX ----
@@ -42,6 +62,10 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int src_bytes) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n"
                  :: "r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+// Full 16-byte copy (interior tiles: no zero-fill operand).
+__device__ __forceinline__ void cp_async16_full(uint32_t dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" :: "r"(dst), "l"(src) : "memory");
 }
 // 4-byte variant (unaligned rows, transposes, tails); src_bytes 0 writes a zero.
 __device__ __forceinline__ void cp_async4(uint32_t dst, const void* src, int src_bytes) {

@@ -32,6 +32,12 @@
 //     oracle (oracle/gemm_ref.c); K/M/N tails are zero-filled in shared memory.
 #pragma once
 
+#include <algorithm>
+#include <map>
+#include <type_traits>
+#include <mutex>
+#include <utility>
+
 #include "kp_internal.cuh"
 
 namespace kp {
@@ -56,12 +62,19 @@ struct Params {
     int M, N, K;
     int64_t lda, ldb, ldc, sa, sb, sc;
     float alpha, beta;
-    int wgr, wgc, log_wgc;
+    int wgr, wgc, log_wgc, log_nthr;
     int log_bm, log_bn;
     int stages;
     int vecA, vecB, vecC;
     int tiles_m, tiles_n;
     int a_elems, b_elems;    // floats per stage (chunk-major tiles)
+    // ordered stream-K (sk != 0): gridDim.x persistent CTAs share
+    // units = tiles*batch*KT (tile, k-slice) units; hand-off flags live in a
+    // ring of KP_SK_RING slots owned by the library
+    int sk;
+    int64_t units, dp_tiles;
+    uint32_t* flags;
+    uint32_t flag_base, epoch;
 };
 
 // Shared-memory tile layout ("chunk-major"): an operand tile of BM (or BN)
@@ -224,9 +237,134 @@ struct Frag {
     }
 };
 
+// Accumulator tile on Blackwell's packed FP32 pipe (FFMA2, `__ffma2_rn`):
+// two C elements share one 64-bit register pair and one instruction updates
+// both with the same single-rounding FMA as fmaf, so the increasing-k fmaf
+// chain of every element (and bit-exactness vs the oracle) is unchanged while
+// the FFMA issue count halves.  Pairs run along the column axis when the B
+// fragment delivers adjacent columns in adjacent registers (B normal, chunk
+// layout), along the row axis when A does (A transposed); when neither
+// fragment has adjacent outputs in adjacent registers (A normal x B
+// transposed: both are k-vector row layouts) pairing would cost a register
+// move per FFMA2, so that layout (and a 1x1 tile) stays on scalar FFMA.  The
+// broadcast operand costs nothing: ptxas folds make_float2(x, x) into FFMA2's
+// scalar-operand form.
+template <int RT, int CT, bool TA, bool TB>
+struct AccTile {
+    static constexpr int PAIR = (!TB && CT >= 2) ? 1 : (TA && RT >= 2) ? 2 : 0;  // 1: column pairs, 2: row pairs
+    static constexpr int PR = PAIR == 2 ? RT / 2 : RT;
+    static constexpr int PC = PAIR == 1 ? CT / 2 : CT;
+    using Elem = typename std::conditional<PAIR == 0, float, float2>::type;
+    Elem v[PR][PC];
+
+    __device__ __forceinline__ float& at(int i, int j) {
+        if constexpr (PAIR == 1) return (j & 1) ? v[i][j >> 1].y : v[i][j >> 1].x;
+        else if constexpr (PAIR == 2) return (i & 1) ? v[i >> 1][j].y : v[i >> 1][j].x;
+        else return v[i][j];
+    }
+    template <int ACC>
+    __device__ __forceinline__ void fma(const float (&a)[ACC][RT], const float (&b)[ACC][CT]) {
+#pragma unroll
+        for (int kk = 0; kk < ACC; ++kk) {
+            if constexpr (PAIR == 1) {
+#pragma unroll
+                for (int i = 0; i < RT; ++i)
+#pragma unroll
+                    for (int jp = 0; jp < PC; ++jp)
+                        v[i][jp] = __ffma2_rn(make_float2(a[kk][i], a[kk][i]),
+                                              make_float2(b[kk][2 * jp], b[kk][2 * jp + 1]), v[i][jp]);
+            } else if constexpr (PAIR == 2) {
+#pragma unroll
+                for (int ip = 0; ip < PR; ++ip)
+#pragma unroll
+                    for (int j = 0; j < CT; ++j)
+                        v[ip][j] = __ffma2_rn(make_float2(a[kk][2 * ip], a[kk][2 * ip + 1]),
+                                              make_float2(b[kk][j], b[kk][j]), v[ip][j]);
+            } else {
+#pragma unroll
+                for (int i = 0; i < RT; ++i)
+#pragma unroll
+                    for (int j = 0; j < CT; ++j) v[i][j] = fmaf(a[kk][i], b[kk][j], v[i][j]);
+            }
+        }
+    }
+};
+
 __device__ __forceinline__ float epilogue(float acc, float alpha, float beta, const float* c_old) {
     const float v = alpha * acc;
     return beta == 0.0f ? v : fmaf(beta, *c_old, v);
+}
+
+// Interior-tile copies (no M/N/K tail, 16-byte aligned rows): fixed 16-byte
+// cp.async, the per-thread pointers advance by a constant stride, no zero-fill
+// size arithmetic.  Same shared layouts as copy_rows / copy_direct.
+template <int BK>
+__device__ __forceinline__ void copy_rows_full(uint32_t s, const float* src, int64_t ld,
+                                               int log_rows, int tid, int log_nthr) {
+    constexpr int RS = Geo<BK>::RS, TPR = BK / 4, LOG_TPR = BK == 32 ? 3 : 2;
+    const int r0 = tid >> LOG_TPR, c0 = (tid & (TPR - 1)) << 2;
+    const int log_dr = log_nthr - LOG_TPR;
+    // rows and dr are powers of two: n = rows/dr copies, or one for r0 < rows
+    const int n = log_rows >= log_dr ? 1 << (log_rows - log_dr) : int(r0 < (1 << log_rows));
+    const float* gp = src + (int64_t)r0 * ld + c0;
+    uint32_t sp = s + 4u * (r0 * RS + c0);
+    const int64_t gstep = ld << log_dr;
+    const uint32_t sstep = (4u * RS) << log_dr;
+#pragma unroll 2
+    for (int i = 0; i < n; ++i) {
+        cp_async16_full(sp, gp);
+        gp += gstep;
+        sp += sstep;
+    }
+}
+
+template <int BK>
+__device__ __forceinline__ void copy_direct_full(uint32_t s, const float* src, int64_t ld,
+                                                 int log_cols, int tid, int log_nthr) {
+    const int log_cpr = log_cols - 2;  // float4s per K row
+    if (log_nthr >= log_cpr) {  // every copy of this thread sits in one column, dr K-rows apart
+        const int log_dr = log_nthr - log_cpr;
+        const int r0 = tid >> log_cpr, c0 = (tid & ((1 << log_cpr) - 1)) << 2;
+        const int n = Geo<BK>::LOG_BK >= log_dr ? 1 << (Geo<BK>::LOG_BK - log_dr) : int(r0 < BK);
+        const float* gp = src + (int64_t)r0 * ld + c0;
+        uint32_t sp = s + 4u * chunk_off<BK>(r0, c0);
+        const int64_t gstep = ld << log_dr;
+        const uint32_t sstep = 16u << log_dr;
+#pragma unroll 2
+        for (int i = 0; i < n; ++i) {
+            cp_async16_full(sp, gp);
+            gp += gstep;
+            sp += sstep;
+        }
+        return;
+    }
+    // wide tiles: more float4s per K row than threads
+    const int total = BK << log_cpr, nthr = 1 << log_nthr;
+    for (int idx = tid; idx < total; idx += nthr) {
+        const int r = idx >> log_cpr;
+        const int c = (idx & ((1 << log_cpr) - 1)) << 2;
+        cp_async16_full(s + 4u * chunk_off<BK>(r, c), src + (int64_t)r * ld + c);
+    }
+}
+
+// Ordered stream-K hand-off.  A tile split between CTAs c and c+1 is computed
+// k-slices [0, j) by c and [j, KT) by c+1; c writes its raw accumulators into
+// the C tile (beta == 0, so C is scratch until its final write) and publishes
+// `epoch` in its flag; c+1 starts from those accumulators.  The fmaf order of
+// every C element is therefore the same increasing-k chain as the one-CTA
+// kernel (bit-identical results).
+__device__ __forceinline__ void flag_publish(uint32_t* flag, uint32_t epoch) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;\n" :: "l"(flag), "r"(epoch) : "memory");
+}
+__device__ __forceinline__ void flag_wait(const uint32_t* flag, uint32_t epoch) {
+    const long long t0 = clock64();
+    while (true) {
+        uint32_t v;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(flag) : "memory");
+        if (v == epoch) return;
+        if (clock64() - t0 > (1LL << 34)) __trap();  // ~9 s: never hang the GPU
+        __nanosleep(64);
+    }
 }
 
 template <int ACC, int RT, int CT, bool TA, bool TB, int BK>
@@ -240,43 +378,40 @@ __global__ void __launch_bounds__(256, KP_SIMT_MIN_BLOCKS) simt_gemm_kernel(cons
     const int nthr = p.wgr * p.wgc;
     const int ty = tid >> p.log_wgc;
     const int tx = tid & (p.wgc - 1);
-
-    // grouped raster over (tiles_m x tiles_n) for L2 reuse of A rows / B cols
-    const int tile = blockIdx.x;
-    const int per_group = GROUP_M * p.tiles_n;
-    const int group = tile / per_group;
-    const int first_m = group * GROUP_M;
-    const int gsz = min(p.tiles_m - first_m, GROUP_M);
-    const int in_group = tile - group * per_group;
-    const int m0 = (first_m + in_group % gsz) << p.log_bm;
-    const int n0 = (in_group / gsz) << p.log_bn;
-    const int64_t bz = blockIdx.z;
-    const float* __restrict__ A = p.A + bz * p.sa;
-    const float* __restrict__ B = p.B + bz * p.sb;
-    float* __restrict__ C = p.C + bz * p.sc;
+    const int bm = 1 << p.log_bm, bn = 1 << p.log_bn;
 
     float* sA = smem;
     float* sB = smem + p.stages * p.a_elems;
     const uint32_t sA_u = smem_u32(sA), sB_u = smem_u32(sB);
     const int KT = (p.K + BK - 1) >> LOG_BK;
+    const int tiles = p.tiles_m * p.tiles_n;
 
-    auto issue = [&](int kt, int stage) {
-        const int k0 = kt << LOG_BK;
-        const uint32_t a_dst = sA_u + 4u * stage * p.a_elems;
-        const uint32_t b_dst = sB_u + 4u * stage * p.b_elems;
-        if constexpr (TA)   // A stored k x m: rows are K
-            copy_direct<BK>(a_dst, A + (int64_t)k0 * p.lda + m0, p.lda, p.log_bm, p.M - m0,
-                        p.K - k0, p.vecA, tid, nthr);
-        else                // A stored m x k: k-contiguous rows, row layout
-            copy_rows<BK>(a_dst, A + (int64_t)m0 * p.lda + k0, p.lda, p.log_bm, p.M - m0, p.K - k0,
-                      p.vecA, tid, nthr);
-        if constexpr (!TB)  // B stored k x n: rows are K
-            copy_direct<BK>(b_dst, B + (int64_t)k0 * p.ldb + n0, p.ldb, p.log_bn, p.N - n0,
-                        p.K - k0, p.vecB, tid, nthr);
-        else                // B stored n x k: k-contiguous rows, row layout
-            copy_rows<BK>(b_dst, B + (int64_t)n0 * p.ldb + k0, p.ldb, p.log_bn, p.N - n0, p.K - k0,
-                      p.vecB, tid, nthr);
-    };
+    // ---- schedule: which (tile, k-slice range) segments this CTA computes.
+    // Classic: one whole tile per CTA (blockIdx.z = batch).  Ordered stream-K:
+    // CTA c owns units [c*U/G, (c+1)*U/G) of the U = tiles*batch*KT
+    // (tile, k-slice) units; it first computes the leading k-slices of its
+    // last tile (hand-off to c+1), then its whole tiles, then the trailing
+    // k-slices of its first tile (hand-off from c-1, published long before).
+    int64_t full_lo, full_hi, st_tile = -1, fin_tile = -1;
+    int st_ke = 0, fin_kb = 0, n_dp = 0;
+    if (!p.sk) {
+        full_lo = (int64_t)blockIdx.z * tiles + blockIdx.x;
+        full_hi = full_lo + 1;
+    } else {
+        // whole waves first (tiles c, c+G, ... below dp_tiles: neighbouring CTAs
+        // on neighbouring tiles), then the stream-K region of 1-2 waves
+        const int64_t G = gridDim.x, c = blockIdx.x;
+        n_dp = int(p.dp_tiles / G);
+        const int64_t U = p.units - p.dp_tiles * KT;
+        const int64_t u0 = p.dp_tiles * KT + c * U / G, u1 = p.dp_tiles * KT + (c + 1) * U / G;
+        const int64_t tf = u0 / KT, tl = (u1 - 1) / KT;
+        const int kf = int(u0 - tf * KT), ke = int(u1 - tl * KT);
+        full_lo = kf ? tf + 1 : tf;
+        full_hi = ke < KT ? tl : tl + 1;
+        if (ke < KT) { st_tile = tl; st_ke = ke; }
+        if (kf) { fin_tile = tf; fin_kb = kf; }
+    }
+    const int nsteps = n_dp + int(st_tile >= 0) + int(full_hi - full_lo) + int(fin_tile >= 0);
 
     using FragA = Frag<!TA, RT, ACC, BK>;
     using FragB = Frag<TB, CT, ACC, BK>;
@@ -284,80 +419,153 @@ __global__ void __launch_bounds__(256, KP_SIMT_MIN_BLOCKS) simt_gemm_kernel(cons
     FragB fb;
     fa.init(ty, p.wgr);
     fb.init(tx, p.wgc);
-    float acc[RT][CT];
-#pragma unroll
-    for (int i = 0; i < RT; ++i)
-#pragma unroll
-        for (int j = 0; j < CT; ++j) acc[i][j] = 0.0f;
-
     const int S = p.stages;
-    for (int s = 0; s < S - 1; ++s) {
-        if (s < KT) issue(s, s);
-        cp_async_commit();
-    }
 
-    int rd = 0, wr = S - 1;  // stage being read / written
-    for (int kt = 0; kt < KT; ++kt) {
-        if (S == 3) cp_async_wait<1>(); else cp_async_wait<0>();
-        __syncthreads();
-        if (kt + S - 1 < KT) issue(kt + S - 1, wr);
-        cp_async_commit();
-        wr = (wr + 1 == S) ? 0 : wr + 1;
-        const float* a_s = sA + rd * p.a_elems;
-        const float* b_s = sB + rd * p.b_elems;
-        rd = (rd + 1 == S) ? 0 : rd + 1;
-#pragma unroll
-        for (int kb = 0; kb < BK; kb += ACC) {
-            float a[ACC][RT];
-            float b[ACC][CT];
-            fa.load(a_s, kb, a);
-            fb.load(b_s, kb, b);
-#pragma unroll
-            for (int kk = 0; kk < ACC; ++kk)
-#pragma unroll
-                for (int i = 0; i < RT; ++i)
-#pragma unroll
-                    for (int j = 0; j < CT; ++j) acc[i][j] = fmaf(a[kk][i], b[kk][j], acc[i][j]);
+    for (int step = 0; step < nsteps; ++step) {
+        int64_t T;
+        int kb = 0, kend = KT, mode = 0;  // mode 0 whole tile, 1 hand-off out, 2 hand-off in
+        const int sks = step - n_dp;      // step within the stream-K region
+        if (sks < 0) {
+            T = blockIdx.x + (int64_t)step * gridDim.x;
+        } else if (st_tile >= 0 && sks == 0) {
+            T = st_tile; kend = st_ke; mode = 1;
+        } else if (fin_tile >= 0 && step == nsteps - 1) {
+            T = fin_tile; kb = fin_kb; mode = 2;
+        } else {
+            T = full_lo + sks - int(st_tile >= 0);
         }
-    }
-    cp_async_wait<0>();
+        const int64_t bz = T / tiles;
+        const int tile = int(T - bz * tiles);
+        // grouped raster over (tiles_m x tiles_n) for L2 reuse of A rows / B cols
+        const int per_group = GROUP_M * p.tiles_n;
+        const int group = tile / per_group;
+        const int first_m = group * GROUP_M;
+        const int gsz = min(p.tiles_m - first_m, GROUP_M);
+        const int in_group = tile - group * per_group;
+        const int m0 = (first_m + in_group % gsz) << p.log_bm;
+        const int n0 = (in_group / gsz) << p.log_bn;
+        const float* __restrict__ A = p.A + bz * p.sa;
+        const float* __restrict__ B = p.B + bz * p.sb;
+        float* __restrict__ C = p.C + bz * p.sc;
+        const bool fullA = p.vecA && m0 + bm <= p.M;
+        const bool fullB = p.vecB && n0 + bn <= p.N;
 
-    // epilogue: C = alpha*acc (+ beta*C)
+        auto issue = [&](int kt, int stage) {
+            const int k0 = kt << LOG_BK;
+            const uint32_t a_dst = sA_u + 4u * stage * p.a_elems;
+            const uint32_t b_dst = sB_u + 4u * stage * p.b_elems;
+            const bool kfull = k0 + BK <= p.K;
+            if constexpr (TA) {  // A stored k x m: rows are K
+                const float* src = A + (int64_t)k0 * p.lda + m0;
+                if (fullA && kfull) copy_direct_full<BK>(a_dst, src, p.lda, p.log_bm, tid, p.log_nthr);
+                else copy_direct<BK>(a_dst, src, p.lda, p.log_bm, p.M - m0, p.K - k0, p.vecA, tid, nthr);
+            } else {             // A stored m x k: k-contiguous rows, row layout
+                const float* src = A + (int64_t)m0 * p.lda + k0;
+                if (fullA && kfull) copy_rows_full<BK>(a_dst, src, p.lda, p.log_bm, tid, p.log_nthr);
+                else copy_rows<BK>(a_dst, src, p.lda, p.log_bm, p.M - m0, p.K - k0, p.vecA, tid, nthr);
+            }
+            if constexpr (!TB) { // B stored k x n: rows are K
+                const float* src = B + (int64_t)k0 * p.ldb + n0;
+                if (fullB && kfull) copy_direct_full<BK>(b_dst, src, p.ldb, p.log_bn, tid, p.log_nthr);
+                else copy_direct<BK>(b_dst, src, p.ldb, p.log_bn, p.N - n0, p.K - k0, p.vecB, tid, nthr);
+            } else {             // B stored n x k: k-contiguous rows, row layout
+                const float* src = B + (int64_t)n0 * p.ldb + k0;
+                if (fullB && kfull) copy_rows_full<BK>(b_dst, src, p.ldb, p.log_bn, tid, p.log_nthr);
+                else copy_rows<BK>(b_dst, src, p.ldb, p.log_bn, p.N - n0, p.K - k0, p.vecB, tid, nthr);
+            }
+        };
+
+        if (step > 0) __syncthreads();  // every warp is done reading the previous segment's stages
+        for (int s = 0; s < S - 1; ++s) {
+            if (kb + s < kend) issue(kb + s, s);
+            cp_async_commit();
+        }
+
+        AccTile<RT, CT, TA, TB> acc;
+        if (mode == 2) {  // continue the k chain of CTA blockIdx.x - 1
+            if (tid == 0) flag_wait(p.flags + ((p.flag_base + blockIdx.x - 1) & KP_SK_RING_MASK), p.epoch);
+            __syncthreads();
 #pragma unroll
-    for (int i = 0; i < RT; ++i) {
-        const int m = m0 + FragA::index(i, ty, p.wgr);
-        if (m >= p.M) continue;
-        float* crow = C + (int64_t)m * p.ldc;
-        if constexpr (!TB && CT >= 4) {
+            for (int i = 0; i < RT; ++i) {
+                const int m = m0 + FragA::index(i, ty, p.wgr);
 #pragma unroll
-            for (int q = 0; q < CT / 4; ++q) {
-                const int n = n0 + q * 4 * p.wgc + tx * 4;
-                if (p.vecC && n + 3 < p.N) {
-                    float4 v;
-                    if (p.beta == 0.0f) {
-                        v = make_float4(p.alpha * acc[i][4 * q], p.alpha * acc[i][4 * q + 1],
-                                        p.alpha * acc[i][4 * q + 2], p.alpha * acc[i][4 * q + 3]);
-                    } else {
-                        const float4 o = *reinterpret_cast<const float4*>(crow + n);
-                        v = make_float4(fmaf(p.beta, o.x, p.alpha * acc[i][4 * q]),
-                                        fmaf(p.beta, o.y, p.alpha * acc[i][4 * q + 1]),
-                                        fmaf(p.beta, o.z, p.alpha * acc[i][4 * q + 2]),
-                                        fmaf(p.beta, o.w, p.alpha * acc[i][4 * q + 3]));
-                    }
-                    *reinterpret_cast<float4*>(crow + n) = v;
-                } else {
-#pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        if (n + e < p.N)
-                            crow[n + e] = epilogue(acc[i][4 * q + e], p.alpha, p.beta, crow + n + e);
+                for (int j = 0; j < CT; ++j) {
+                    const int n = n0 + FragB::index(j, tx, p.wgc);
+                    acc.at(i, j) = (m < p.M && n < p.N) ? __ldcg(C + (int64_t)m * p.ldc + n) : 0.0f;
                 }
             }
         } else {
 #pragma unroll
-            for (int j = 0; j < CT; ++j) {
-                const int n = n0 + FragB::index(j, tx, p.wgc);
-                if (n < p.N) crow[n] = epilogue(acc[i][j], p.alpha, p.beta, crow + n);
+            for (int i = 0; i < RT; ++i)
+#pragma unroll
+                for (int j = 0; j < CT; ++j) acc.at(i, j) = 0.0f;
+        }
+
+        int rd = 0, wr = S - 1;  // stage being read / written
+        for (int kt = kb; kt < kend; ++kt) {
+            if (S == 3) cp_async_wait<1>(); else cp_async_wait<0>();
+            __syncthreads();
+            if (kt + S - 1 < kend) issue(kt + S - 1, wr);
+            cp_async_commit();
+            wr = (wr + 1 == S) ? 0 : wr + 1;
+            const float* a_s = sA + rd * p.a_elems;
+            const float* b_s = sB + rd * p.b_elems;
+            rd = (rd + 1 == S) ? 0 : rd + 1;
+#pragma unroll
+            for (int kq = 0; kq < BK; kq += ACC) {
+                float a[ACC][RT];
+                float b[ACC][CT];
+                fa.load(a_s, kq, a);
+                fb.load(b_s, kq, b);
+                acc.template fma<ACC>(a, b);
             }
+        }
+        cp_async_wait<0>();
+
+        // epilogue: C = alpha*acc (+ beta*C); a hand-off stores the raw chain
+        const float alpha = mode == 1 ? 1.0f : p.alpha;
+        const float beta = mode == 1 ? 0.0f : p.beta;
+#pragma unroll
+        for (int i = 0; i < RT; ++i) {
+            const int m = m0 + FragA::index(i, ty, p.wgr);
+            if (m >= p.M) continue;
+            float* crow = C + (int64_t)m * p.ldc;
+            if constexpr (!TB && CT >= 4) {
+#pragma unroll
+                for (int q = 0; q < CT / 4; ++q) {
+                    const int n = n0 + q * 4 * p.wgc + tx * 4;
+                    if (p.vecC && n + 3 < p.N) {
+                        float4 v;
+                        if (beta == 0.0f) {
+                            v = make_float4(alpha * acc.at(i, 4 * q), alpha * acc.at(i, 4 * q + 1),
+                                            alpha * acc.at(i, 4 * q + 2), alpha * acc.at(i, 4 * q + 3));
+                        } else {
+                            const float4 o = *reinterpret_cast<const float4*>(crow + n);
+                            v = make_float4(fmaf(beta, o.x, alpha * acc.at(i, 4 * q)),
+                                            fmaf(beta, o.y, alpha * acc.at(i, 4 * q + 1)),
+                                            fmaf(beta, o.z, alpha * acc.at(i, 4 * q + 2)),
+                                            fmaf(beta, o.w, alpha * acc.at(i, 4 * q + 3)));
+                        }
+                        *reinterpret_cast<float4*>(crow + n) = v;
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 4; ++e)
+                            if (n + e < p.N)
+                                crow[n + e] = epilogue(acc.at(i, 4 * q + e), alpha, beta, crow + n + e);
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < CT; ++j) {
+                    const int n = n0 + FragB::index(j, tx, p.wgc);
+                    if (n < p.N) crow[n] = epilogue(acc.at(i, j), alpha, beta, crow + n);
+                }
+            }
+        }
+        if (mode == 1) {  // publish the partial chain to CTA blockIdx.x + 1
+            __threadfence();
+            __syncthreads();
+            if (tid == 0) flag_publish(p.flags + ((p.flag_base + blockIdx.x) & KP_SK_RING_MASK), p.epoch);
         }
     }
 }
@@ -412,7 +620,7 @@ kp_status launch(const GemmProblem& g, int wgr, int wgc, cudaStream_t stream) {
     p.lda = g.lda; p.ldb = g.ldb; p.ldc = g.ldc;
     p.sa = g.sa; p.sb = g.sb; p.sc = g.sc;
     p.alpha = g.alpha; p.beta = g.beta;
-    p.wgr = wgr; p.wgc = wgc; p.log_wgc = ilog2(wgc);
+    p.wgr = wgr; p.wgc = wgc; p.log_wgc = ilog2(wgc); p.log_nthr = ilog2(wgr * wgc);
     p.log_bm = ilog2(bm); p.log_bn = ilog2(bn);
     p.stages = sp.stages;
     const bool multi = g.batch > 1;
@@ -427,8 +635,52 @@ kp_status launch(const GemmProblem& g, int wgr, int wgc, cudaStream_t stream) {
     const int64_t tiles = int64_t(p.tiles_m) * p.tiles_n;
     if (tiles > 0x7fffffffLL || g.batch > 65535)
         return fail(KP_ERR_BAD_SHAPE, "simt: grid too large for this work-group tile");
+    const int nthr = wgr * wgc;
+    p.sk = 0; p.units = 0; p.dp_tiles = 0; p.flags = nullptr; p.flag_base = 0; p.epoch = 0;
     dim3 grid(unsigned(tiles), 1, unsigned(g.batch));
-    kern<<<grid, wgr * wgc, sp.bytes, stream>>>(p);
+    // Ordered stream-K (see simt_gemm_kernel): spread the tile x k-slice
+    // units evenly over one persistent wave when whole tiles would leave part
+    // of the last wave idle.  beta == 0 only (C doubles as the hand-off
+    // buffer); at least one k-slice range per CTA, so a tile is split between
+    // at most two CTAs and no CTA waits on a chain.
+    const int sched = simt_schedule();
+    const int64_t T = tiles * g.batch;
+    const int64_t KT = (g.k + sp.bk - 1) / sp.bk;
+    if (sched != 0 && g.beta == 0.0f && T >= 2 && KT >= 2 && T * KT < (int64_t(1) << 40)) {
+        static std::mutex mu;
+        static std::map<std::pair<int, size_t>, int> occ_cache;
+        int occ = 0;
+        {
+            std::lock_guard<std::mutex> lock(mu);
+            auto it = occ_cache.find({nthr, sp.bytes});
+            if (it == occ_cache.end()) {
+                if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nthr, sp.bytes) != cudaSuccess)
+                    return check_launch("cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+                occ_cache[{nthr, sp.bytes}] = occ;
+            } else {
+                occ = it->second;
+            }
+        }
+        const int64_t slots = int64_t(sm_count()) * occ;
+        int64_t G = 0, dp = 0;
+        if (sched == 2) {
+            G = std::min(slots, T - 1);
+        } else if (T > slots && T < 2 * slots && occ <= 2) {
+            // Measured policy (tools/k1_ab.py, profiles/): pays only for a
+            // ragged second wave of big (>= 256-thread, <= 2 per SM) CTAs;
+            // with more waves, or smaller CTAs, the hardware's own refill of
+            // the SMs that finish early already balances the tail.
+            if (double(T) / double(2 * slots) < 0.95) G = slots;
+        }
+        if (G >= 1 && slots >= 1) {
+            SkFlags f;
+            kp_status st = sk_reserve(uint32_t(G), &f);
+            if (st != KP_OK) return st;
+            p.sk = 1; p.units = T * KT; p.dp_tiles = dp; p.flags = f.flags; p.flag_base = f.base; p.epoch = f.epoch;
+            grid = dim3(unsigned(G), 1, 1);
+        }
+    }
+    kern<<<grid, nthr, sp.bytes, stream>>>(p);
     note_launch();
     return check_launch("simt_gemm_kernel");
 }

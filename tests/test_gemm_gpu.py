@@ -208,3 +208,91 @@ def test_pinned_pipeline_matches_device_matmul():
         got = pipe.run(probs)
         for g, w in zip(got, want):
             assert torch.equal(g, w)
+
+
+@pytest.fixture
+def schedule():
+    """Set the K1 tile-scheduling mode (kp_set_schedule) for one test."""
+    from paper_2003_06795_b200 import _native as nat
+    prev = []
+
+    def set_mode(mode):
+        prev.append(nat.lib().kp_set_schedule(mode))
+    yield set_mode
+    if prev:
+        nat.lib().kp_set_schedule(prev[0])
+
+
+@pytest.mark.parametrize("shape,ta,tb", [((70, 200, 66), False, False), ((45, 130, 97), True, True),
+                                         ((64, 64, 64), False, True), ((33, 300, 40), True, False)])
+def test_every_config_bit_exact_forced_stream_k(schedule, shape, ta, tb):
+    """Ordered stream-K forced on small problems (grid = tiles - 1, so tiles
+    are split between neighbouring CTAs): still bit-identical to the
+    sequential-fmaf oracle for every config."""
+    schedule(2)
+    m, k, n = shape
+    rng = np.random.default_rng(11)
+    a_store, b_store, a, b = _operands(rng, m, k, n, ta, tb)
+    want = gemm_f32_exact(a_store, b_store, m=m, k=k, n=n, trans_a=ta, trans_b=tb).reshape(m, n)
+    bad = []
+    for cfg in _dataset().all_configs():
+        got = _gemm().matmul(a, b, cfg).cpu().numpy()
+        if not np.array_equal(got, want):
+            bad.append(cfg.as_tuple())
+    assert not bad, f"{len(bad)} configs differ, first {bad[:5]}"
+
+
+@pytest.mark.parametrize("mkn", [(1500, 777, 1300), (2000, 300, 2000)])
+@pytest.mark.parametrize("cfg", [(1, 8, 8, 32, 8), (4, 8, 4, 16, 16), (2, 4, 4, 16, 16),
+                                 (4, 8, 8, 16, 16), (1, 1, 1, 1, 64)])
+def test_auto_stream_k_large_matches_one_tile_per_cta(schedule, cfg, mkn):
+    """Problems with more tiles than resident CTAs take the stream-K schedule
+    in auto mode (2000^2 with 64x64 tiles: two whole waves, then stream-K over
+    the rest); C must equal the one-tile-per-CTA result bit for bit and the
+    oracle on sampled rows."""
+    gemm = _gemm()
+    m, k, n = mkn
+    rng = np.random.default_rng(12)
+    a_store, b_store, a, b = _operands(rng, m, k, n, False, False)
+    schedule(1)
+    got = gemm.matmul(a, b, cfg).cpu().numpy()
+    schedule(0)
+    classic = gemm.matmul(a, b, cfg).cpu().numpy()
+    np.testing.assert_array_equal(got, classic)
+    rows = np.array([0, 1, 255, 256, 700, 1023, 1024, 1499, m - 1])
+    want = gemm_f32_exact(np.ascontiguousarray(a_store[rows]), b_store, m=len(rows), k=k,
+                          n=n).reshape(len(rows), n)
+    np.testing.assert_array_equal(got[rows], want)
+
+
+def test_stream_k_batched_and_back_to_back(schedule):
+    """Stream-K over a strided batch (units span batch entries) and many
+    back-to-back launches (flag ring reuse) stay exact."""
+    schedule(2)
+    ds = _dataset()
+    rng = np.random.default_rng(13)
+    batch, m, k, n = 5, 96, 160, 80
+    a = rng.uniform(-1, 1, (batch, m, k)).astype(np.float32)
+    b = rng.uniform(-1, 1, (batch, k, n)).astype(np.float32)
+    want = gemm_f32_exact(a, b, m=m, k=k, n=n, batch=batch, stride_a=m * k, stride_b=k * n)
+    ta, tb = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    for cfg in [ds.KernelConfig(4, 4, 4, 8, 8), ds.KernelConfig(2, 2, 8, 16, 8)]:
+        outs = [_gemm().matmul(ta, tb, cfg) for _ in range(300)]
+        for o in outs[::37] + outs[-1:]:
+            np.testing.assert_array_equal(o.cpu().numpy().reshape(-1), want)
+
+
+def test_stream_k_needs_beta_zero(schedule):
+    """beta != 0 keeps the one-tile-per-CTA schedule (C is read), still exact."""
+    schedule(2)
+    ds = _dataset()
+    rng = np.random.default_rng(14)
+    m, k, n = 70, 90, 60
+    a = rng.uniform(-1, 1, (m, k)).astype(np.float32)
+    b = rng.uniform(-1, 1, (k, n)).astype(np.float32)
+    c0 = rng.uniform(-1, 1, (m, n)).astype(np.float32)
+    out = torch.from_numpy(c0.copy()).cuda()
+    _gemm().matmul(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(),
+                   ds.KernelConfig(2, 2, 2, 8, 8), out=out, alpha=2.0, beta=0.5)
+    want = gemm_f32_exact(a, b, m=m, k=k, n=n, alpha=2.0, beta=0.5, c_init=c0)
+    np.testing.assert_array_equal(out.cpu().numpy().reshape(-1), want)
