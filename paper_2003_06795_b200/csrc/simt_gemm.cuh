@@ -21,7 +21,9 @@
 //         output rows x BK K-slices per padded chunk (chunk_off); a thread
 //         owns 4-wide row chunks strided by 4*wg and reads one LDS.128 per
 //         chunk per K slice, and stores C with 16-byte STG;
-//       k-contiguous sources (A normal, B transposed): "row" layout (RS
+//       B transposed: transposed into the chunk layout by 4-byte cp.async
+//         (copy_transpose), so B fragments are always column vectors;
+//       k-contiguous A (A normal): "row" layout (RS
 //         pitch); a thread owns rows t + i*wg and reads K vectors of width
 //         min(acc, 4) per row -- `acc` is the K vector width, as in the
 //         paper's kernel;
@@ -33,6 +35,7 @@
 #pragma once
 
 #include <algorithm>
+#include <cstdlib>
 #include <map>
 #include <type_traits>
 #include <mutex>
@@ -241,17 +244,17 @@ struct Frag {
 // two C elements share one 64-bit register pair and one instruction updates
 // both with the same single-rounding FMA as fmaf, so the increasing-k fmaf
 // chain of every element (and bit-exactness vs the oracle) is unchanged while
-// the FFMA issue count halves.  Pairs run along the column axis when the B
-// fragment delivers adjacent columns in adjacent registers (B normal, chunk
-// layout), along the row axis when A does (A transposed); when neither
-// fragment has adjacent outputs in adjacent registers (A normal x B
-// transposed: both are k-vector row layouts) pairing would cost a register
-// move per FFMA2, so that layout (and a 1x1 tile) stays on scalar FFMA.  The
-// broadcast operand costs nothing: ptxas folds make_float2(x, x) into FFMA2's
+// the FFMA issue count halves.  When B is staged n-contiguous (chunk layout:
+// B normal, or B transposed through copy_transpose) its fragment holds
+// adjacent columns in adjacent registers and pairs run along columns;
+// otherwise pairs run along rows when A is transposed (chunk layout), and the
+// remaining cases (A normal x row-staged B, 1x1 tiles) stay on scalar FFMA --
+// pairing values from different loads would cost a move per FFMA2.  The broadcast
+// operand costs nothing: ptxas folds make_float2(x, x) into FFMA2's
 // scalar-operand form.
-template <int RT, int CT, bool TA, bool TB>
+template <int RT, int CT, bool TA, bool B_CHUNK>
 struct AccTile {
-    static constexpr int PAIR = (!TB && CT >= 2) ? 1 : (TA && RT >= 2) ? 2 : 0;  // 1: column pairs, 2: row pairs
+    static constexpr int PAIR = (B_CHUNK && CT >= 2) ? 1 : (TA && RT >= 2) ? 2 : 0;  // 1: column pairs, 2: row pairs
     static constexpr int PR = PAIR == 2 ? RT / 2 : RT;
     static constexpr int PC = PAIR == 1 ? CT / 2 : CT;
     using Elem = typename std::conditional<PAIR == 0, float, float2>::type;
@@ -347,6 +350,53 @@ __device__ __forceinline__ void copy_direct_full(uint32_t s, const float* src, i
     }
 }
 
+// B stored n x k (k contiguous, B transposed), staged transposed into the
+// chunk layout, so the B fragment is one LDS.128 of 4 adjacent columns per k
+// (FFMA2 column pairs, 16-byte C stores) whatever the operand layout.  4-byte
+// cp.async; consecutive threads take (n & 3) fastest, then k: a warp reads 4
+// rows x 8 consecutive k (whole 32-byte sectors) and writes 32 consecutive
+// shared words (no bank conflict).  Elements with n >= rv or k >= kv are
+// zero-filled unless `full`.
+template <int BK>
+__device__ __forceinline__ void copy_transpose(uint32_t s, const float* src, int64_t ld,
+                                               int log_rows, int rv, int kv, bool full, int tid,
+                                               int log_nthr) {
+    constexpr int LOG_BK = Geo<BK>::LOG_BK;
+    const int rows = 1 << log_rows;
+    if (log_rows >= 2 && log_nthr >= LOG_BK + 2) {  // (k, n & 3) fixed per thread
+        const int nl = tid & 3, k = (tid >> 2) & (BK - 1);
+        const int dn = 1 << (log_nthr - LOG_BK);     // rows advanced per copy (multiple of 4)
+        const int n0 = ((tid >> (LOG_BK + 2)) << 2) + nl;
+        const float* gp = src + (int64_t)n0 * ld + k;
+        uint32_t sp = s + 4u * chunk_off<BK>(k, n0);
+        const int64_t gstep = (int64_t)dn * ld;
+        const uint32_t sstep = 4u * (dn >> 2) * Geo<BK>::CH;
+        if (full) {
+#pragma unroll 4
+            for (int n = n0; n < rows; n += dn) {
+                cp_async4_full(sp, gp);
+                gp += gstep;
+                sp += sstep;
+            }
+        } else {
+            for (int n = n0; n < rows; n += dn) {
+                cp_async4(sp, gp, (n < rv && k < kv) ? 4 : 0);
+                gp += gstep;
+                sp += sstep;
+            }
+        }
+        return;
+    }
+    const int lr = log_rows < 2 ? log_rows : 2;  // low bits of n taken fastest
+    const int total = rows << LOG_BK, nthr = 1 << log_nthr;
+    for (int idx = tid; idx < total; idx += nthr) {
+        const int k = (idx >> lr) & (BK - 1);
+        const int n = ((idx >> (lr + LOG_BK)) << lr) + (idx & ((1 << lr) - 1));
+        cp_async4(s + 4u * chunk_off<BK>(k, n), src + (int64_t)n * ld + k,
+                  (full || (n < rv && k < kv)) ? 4 : 0);
+    }
+}
+
 // Ordered stream-K hand-off.  A tile split between CTAs c and c+1 is computed
 // k-slices [0, j) by c and [j, KT) by c+1; c writes its raw accumulators into
 // the C tile (beta == 0, so C is scratch until its final write) and publishes
@@ -367,7 +417,9 @@ __device__ __forceinline__ void flag_wait(const uint32_t* flag, uint32_t epoch) 
     }
 }
 
-template <int ACC, int RT, int CT, bool TA, bool TB, int BK>
+// BT (B transposed only): stage B transposed into the chunk layout (true) or
+// keep its k-contiguous rows (false); chosen per problem by launch().
+template <int ACC, int RT, int CT, bool TA, bool TB, int BK, bool BT>
 #ifndef KP_SIMT_MIN_BLOCKS
 #define KP_SIMT_MIN_BLOCKS 2
 #endif
@@ -414,7 +466,8 @@ __global__ void __launch_bounds__(256, KP_SIMT_MIN_BLOCKS) simt_gemm_kernel(cons
     const int nsteps = n_dp + int(st_tile >= 0) + int(full_hi - full_lo) + int(fin_tile >= 0);
 
     using FragA = Frag<!TA, RT, ACC, BK>;
-    using FragB = Frag<TB, CT, ACC, BK>;
+    constexpr bool B_CHUNK = !TB || BT;  // B staged n-contiguous
+    using FragB = Frag<!B_CHUNK, CT, ACC, BK>;
     FragA fa;
     FragB fb;
     fa.init(ty, p.wgr);
@@ -468,6 +521,9 @@ __global__ void __launch_bounds__(256, KP_SIMT_MIN_BLOCKS) simt_gemm_kernel(cons
                 const float* src = B + (int64_t)k0 * p.ldb + n0;
                 if (fullB && kfull) copy_direct_full<BK>(b_dst, src, p.ldb, p.log_bn, tid, p.log_nthr);
                 else copy_direct<BK>(b_dst, src, p.ldb, p.log_bn, p.N - n0, p.K - k0, p.vecB, tid, nthr);
+            } else if constexpr (BT) {  // B stored n x k, transposed into the chunk layout
+                copy_transpose<BK>(b_dst, B + (int64_t)n0 * p.ldb + k0, p.ldb, p.log_bn, p.N - n0,
+                                   p.K - k0, n0 + bn <= p.N && kfull, tid, p.log_nthr);
             } else {             // B stored n x k: k-contiguous rows, row layout
                 const float* src = B + (int64_t)n0 * p.ldb + k0;
                 if (fullB && kfull) copy_rows_full<BK>(b_dst, src, p.ldb, p.log_bn, tid, p.log_nthr);
@@ -481,7 +537,7 @@ __global__ void __launch_bounds__(256, KP_SIMT_MIN_BLOCKS) simt_gemm_kernel(cons
             cp_async_commit();
         }
 
-        AccTile<RT, CT, TA, TB> acc;
+        AccTile<RT, CT, TA, B_CHUNK> acc;
         if (mode == 2) {  // continue the k chain of CTA blockIdx.x - 1
             if (tid == 0) flag_wait(p.flags + ((p.flag_base + blockIdx.x - 1) & KP_SK_RING_MASK), p.epoch);
             __syncthreads();
@@ -530,7 +586,7 @@ __global__ void __launch_bounds__(256, KP_SIMT_MIN_BLOCKS) simt_gemm_kernel(cons
             const int m = m0 + FragA::index(i, ty, p.wgr);
             if (m >= p.M) continue;
             float* crow = C + (int64_t)m * p.ldc;
-            if constexpr (!TB && CT >= 4) {
+            if constexpr (B_CHUNK && CT >= 4) {
 #pragma unroll
                 for (int q = 0; q < CT / 4; ++q) {
                     const int n = n0 + q * 4 * p.wgc + tx * 4;
@@ -602,15 +658,24 @@ inline SmemPlan plan_smem(bool a_rows, bool b_rows, int bm, int bn) {
 template <int ACC, int RT, int CT, bool TA, bool TB>
 kp_status launch(const GemmProblem& g, int wgr, int wgc, cudaStream_t stream) {
     const int bm = RT * wgr, bn = CT * wgc;
-    const SmemPlan sp = plan_smem(!TA, TB, bm, bn);
+    // B transposed: stage it transposed (FFMA2 column pairs, 4-byte copies)
+    // only for tall problems; measured on the network+squares NT sweep, the
+    // transposing copy wins +11 % geomean at m >= 4096, breaks even at
+    // 1024-4095 and loses 4-9 % below (copy-bound, small m).
+    const bool bt = TB && g.m >= 2048;
+    const SmemPlan sp = plan_smem(!TA, TB && !bt, bm, bn);
     if (sp.bytes > 227 * 1024) return fail(KP_ERR_UNSUPPORTED, "simt: shared-memory plan too large");
-    auto kern = sp.bk == 32 ? simt_gemm_kernel<ACC, RT, CT, TA, TB, 32>
-                            : simt_gemm_kernel<ACC, RT, CT, TA, TB, 16>;
-    static bool attr_done[2] = {false, false};  // idempotent; one process drives one device
-    if (!attr_done[sp.bk == 32]) {
+    void (*kern)(const Params) = sp.bk == 32 ? simt_gemm_kernel<ACC, RT, CT, TA, TB, 32, false>
+                                             : simt_gemm_kernel<ACC, RT, CT, TA, TB, 16, false>;
+    if constexpr (TB) {
+        if (bt) kern = sp.bk == 32 ? simt_gemm_kernel<ACC, RT, CT, TA, TB, 32, true>
+                                   : simt_gemm_kernel<ACC, RT, CT, TA, TB, 16, true>;
+    }
+    static bool attr_done[2][2] = {{false, false}, {false, false}};  // one process drives one device
+    if (!attr_done[sp.bk == 32][bt]) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
             return check_launch("cudaFuncSetAttribute");
-        attr_done[sp.bk == 32] = true;
+        attr_done[sp.bk == 32][bt] = true;
     }
     Params p;
     p.A = static_cast<const float*>(g.A);
@@ -652,15 +717,21 @@ kp_status launch(const GemmProblem& g, int wgr, int wgc, cudaStream_t stream) {
         int occ = 0;
         {
             std::lock_guard<std::mutex> lock(mu);
-            auto it = occ_cache.find({nthr, sp.bytes});
+            auto it = occ_cache.find({nthr * 2 + int(bt), sp.bytes});
             if (it == occ_cache.end()) {
                 if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nthr, sp.bytes) != cudaSuccess)
                     return check_launch("cudaOccupancyMaxActiveBlocksPerMultiprocessor");
-                occ_cache[{nthr, sp.bytes}] = occ;
+                occ_cache[{nthr * 2 + int(bt), sp.bytes}] = occ;
             } else {
                 occ = it->second;
             }
         }
+        // KP_SK_OCC (tuning experiments only): cap the stream-K CTAs per SM
+        static const int occ_cap = [] {
+            const char* e = std::getenv("KP_SK_OCC");
+            return e ? std::atoi(e) : 0;
+        }();
+        if (occ_cap > 0 && occ > occ_cap) occ = occ_cap;
         const int64_t slots = int64_t(sm_count()) * occ;
         int64_t G = 0, dp = 0;
         if (sched == 2) {

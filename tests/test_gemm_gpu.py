@@ -296,3 +296,19 @@ def test_stream_k_needs_beta_zero(schedule):
                    ds.KernelConfig(2, 2, 2, 8, 8), out=out, alpha=2.0, beta=0.5)
     want = gemm_f32_exact(a, b, m=m, k=k, n=n, alpha=2.0, beta=0.5, c_init=c0)
     np.testing.assert_array_equal(out.cpu().numpy().reshape(-1), want)
+
+
+@pytest.mark.parametrize("ta", [False, True])
+def test_every_config_bit_exact_tall_b_transposed(ta):
+    """m >= 2048 with B transposed stages B transposed into the chunk layout
+    (copy_transpose, FFMA2 column pairs); ragged m/n/k edges included."""
+    m, k, n = 2053, 45, 37
+    rng = np.random.default_rng(15)
+    a_store, b_store, a, b = _operands(rng, m, k, n, ta, True)
+    want = gemm_f32_exact(a_store, b_store, m=m, k=k, n=n, trans_a=ta, trans_b=True).reshape(m, n)
+    bad = []
+    for cfg in _dataset().all_configs():
+        got = _gemm().matmul(a, b, cfg).cpu().numpy()
+        if not np.array_equal(got, want):
+            bad.append(cfg.as_tuple())
+    assert not bad, f"{len(bad)} configs differ, first {bad[:5]}"
