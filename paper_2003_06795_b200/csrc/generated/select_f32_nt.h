@@ -16,383 +16,473 @@ static inline select_f32_nt_config select_f32_nt(int64_t m, int64_t k, int64_t n
     (void)k;
     (void)n;
     if (m < INT64_C(2218)) {
-        if (m < INT64_C(112)) {
-            if (k < INT64_C(544)) {
-                if (k < INT64_C(405)) {
-                    select_f32_nt_config out = {8u, 4u, 1u, 8u, 8u};
+        if (m < INT64_C(12)) {
+            if (n < INT64_C(2024)) {
+                if (k < INT64_C(2897)) {
+                    select_f32_nt_config out = {8u, 1u, 1u, 8u, 8u};
                     return out;
                 } else {
-                    if (m < INT64_C(70)) {
-                        select_f32_nt_config out = {8u, 4u, 1u, 8u, 8u};
+                    if (m < INT64_C(3)) {
+                        select_f32_nt_config out = {8u, 1u, 1u, 8u, 8u};
                         return out;
                     } else {
-                        select_f32_nt_config out = {8u, 4u, 4u, 16u, 8u};
+                        select_f32_nt_config out = {4u, 1u, 1u, 8u, 8u};
                         return out;
                     }
                 }
             } else {
-                if (n < INT64_C(1432)) {
-                    select_f32_nt_config out = {8u, 1u, 1u, 8u, 8u};
-                    return out;
-                } else {
-                    if (m < INT64_C(29)) {
-                        select_f32_nt_config out = {8u, 1u, 1u, 8u, 8u};
+                if (m < INT64_C(6)) {
+                    if (m < INT64_C(2)) {
+                        select_f32_nt_config out = {4u, 1u, 1u, 8u, 8u};
                         return out;
                     } else {
-                        if (m < INT64_C(70)) {
-                            select_f32_nt_config out = {8u, 4u, 1u, 8u, 8u};
-                            return out;
-                        } else {
-                            select_f32_nt_config out = {2u, 4u, 4u, 8u, 8u};
-                            return out;
-                        }
+                        select_f32_nt_config out = {8u, 1u, 1u, 8u, 8u};
+                        return out;
                     }
+                } else {
+                    select_f32_nt_config out = {4u, 1u, 1u, 8u, 8u};
+                    return out;
                 }
             }
         } else {
-            if (n < INT64_C(744)) {
-                if (n < INT64_C(176)) {
-                    if (m < INT64_C(555)) {
-                        if (k < INT64_C(471)) {
-                            if (m < INT64_C(159)) {
-                                select_f32_nt_config out = {8u, 4u, 1u, 8u, 8u};
-                                return out;
+            if (n < INT64_C(176)) {
+                if (m < INT64_C(555)) {
+                    if (m < INT64_C(80)) {
+                        if (m < INT64_C(57)) {
+                            select_f32_nt_config out = {4u, 1u, 1u, 8u, 8u};
+                            return out;
+                        } else {
+                            select_f32_nt_config out = {4u, 2u, 2u, 8u, 8u};
+                            return out;
+                        }
+                    } else {
+                        if (n < INT64_C(144)) {
+                            if (k < INT64_C(471)) {
+                                if (m < INT64_C(159)) {
+                                    select_f32_nt_config out = {8u, 1u, 1u, 8u, 8u};
+                                    return out;
+                                } else {
+                                    if (m < INT64_C(278)) {
+                                        select_f32_nt_config out = {4u, 2u, 1u, 8u, 8u};
+                                        return out;
+                                    } else {
+                                        if (n < INT64_C(79)) {
+                                            select_f32_nt_config out = {8u, 1u, 1u, 8u, 8u};
+                                            return out;
+                                        } else {
+                                            select_f32_nt_config out = {4u, 2u, 1u, 8u, 8u};
+                                            return out;
+                                        }
+                                    }
+                                }
                             } else {
                                 select_f32_nt_config out = {8u, 1u, 1u, 8u, 8u};
                                 return out;
                             }
                         } else {
-                            if (k < INT64_C(744)) {
-                                select_f32_nt_config out = {8u, 4u, 1u, 8u, 8u};
+                            if (m < INT64_C(139)) {
+                                if (k < INT64_C(744)) {
+                                    select_f32_nt_config out = {4u, 2u, 1u, 8u, 8u};
+                                    return out;
+                                } else {
+                                    select_f32_nt_config out = {8u, 1u, 1u, 8u, 8u};
+                                    return out;
+                                }
+                            } else {
+                                select_f32_nt_config out = {4u, 2u, 1u, 8u, 8u};
+                                return out;
+                            }
+                        }
+                    }
+                } else {
+                    if (k < INT64_C(222)) {
+                        if (m < INT64_C(1109)) {
+                            select_f32_nt_config out = {4u, 2u, 2u, 8u, 8u};
+                            return out;
+                        } else {
+                            if (k < INT64_C(167)) {
+                                select_f32_nt_config out = {4u, 2u, 2u, 8u, 8u};
                                 return out;
                             } else {
-                                select_f32_nt_config out = {8u, 1u, 1u, 8u, 8u};
-                                return out;
+                                if (n < INT64_C(46)) {
+                                    select_f32_nt_config out = {4u, 1u, 1u, 8u, 8u};
+                                    return out;
+                                } else {
+                                    select_f32_nt_config out = {4u, 2u, 2u, 8u, 8u};
+                                    return out;
+                                }
                             }
                         }
                     } else {
                         if (k < INT64_C(444)) {
-                            if (m < INT64_C(1109)) {
-                                if (n < INT64_C(46)) {
-                                    select_f32_nt_config out = {8u, 1u, 1u, 8u, 8u};
+                            if (k < INT64_C(314)) {
+                                select_f32_nt_config out = {4u, 2u, 1u, 8u, 8u};
+                                return out;
+                            } else {
+                                select_f32_nt_config out = {4u, 2u, 1u, 8u, 8u};
+                                return out;
+                            }
+                        } else {
+                            if (k < INT64_C(1052)) {
+                                select_f32_nt_config out = {4u, 2u, 2u, 8u, 8u};
+                                return out;
+                            } else {
+                                if (m < INT64_C(1109)) {
+                                    select_f32_nt_config out = {4u, 2u, 1u, 8u, 8u};
                                     return out;
                                 } else {
-                                    if (k < INT64_C(314)) {
-                                        select_f32_nt_config out = {8u, 4u, 1u, 8u, 8u};
+                                    select_f32_nt_config out = {4u, 2u, 2u, 8u, 8u};
+                                    return out;
+                                }
+                            }
+                        }
+                    }
+                }
+            } else {
+                if (m < INT64_C(448)) {
+                    if (n < INT64_C(1012)) {
+                        if (m < INT64_C(317)) {
+                            if (k < INT64_C(1145)) {
+                                if (n < INT64_C(444)) {
+                                    if (m < INT64_C(139)) {
+                                        select_f32_nt_config out = {8u, 1u, 1u, 8u, 8u};
                                         return out;
                                     } else {
-                                        if (n < INT64_C(79)) {
-                                            select_f32_nt_config out = {8u, 4u, 1u, 8u, 8u};
-                                            return out;
+                                        if (m < INT64_C(224)) {
+                                            if (k < INT64_C(182)) {
+                                                select_f32_nt_config out = {4u, 2u, 1u, 8u, 8u};
+                                                return out;
+                                            } else {
+                                                if (k < INT64_C(725)) {
+                                                    select_f32_nt_config out = {4u, 2u, 2u, 8u, 8u};
+                                                    return out;
+                                                } else {
+                                                    select_f32_nt_config out = {4u, 2u, 1u, 8u, 8u};
+                                                    return out;
+                                                }
+                                            }
                                         } else {
                                             select_f32_nt_config out = {8u, 1u, 1u, 8u, 8u};
                                             return out;
                                         }
                                     }
-                                }
-                            } else {
-                                select_f32_nt_config out = {8u, 4u, 1u, 8u, 8u};
-                                return out;
-                            }
-                        } else {
-                            if (m < INT64_C(1109)) {
-                                select_f32_nt_config out = {8u, 4u, 1u, 8u, 8u};
-                                return out;
-                            } else {
-                                if (n < INT64_C(111)) {
-                                    select_f32_nt_config out = {8u, 4u, 1u, 8u, 8u};
-                                    return out;
                                 } else {
-                                    select_f32_nt_config out = {4u, 4u, 4u, 8u, 8u};
-                                    return out;
-                                }
-                            }
-                        }
-                    }
-                } else {
-                    if (m < INT64_C(448)) {
-                        if (k < INT64_C(157)) {
-                            if (m < INT64_C(278)) {
-                                select_f32_nt_config out = {8u, 4u, 1u, 8u, 8u};
-                                return out;
-                            } else {
-                                select_f32_nt_config out = {4u, 4u, 4u, 8u, 8u};
-                                return out;
-                            }
-                        } else {
-                            if (n < INT64_C(287)) {
-                                if (m < INT64_C(224)) {
-                                    if (k < INT64_C(725)) {
-                                        select_f32_nt_config out = {8u, 4u, 1u, 8u, 8u};
+                                    if (m < INT64_C(70)) {
+                                        select_f32_nt_config out = {4u, 1u, 1u, 8u, 8u};
                                         return out;
                                     } else {
-                                        select_f32_nt_config out = {8u, 1u, 1u, 8u, 8u};
+                                        select_f32_nt_config out = {4u, 2u, 2u, 8u, 8u};
                                         return out;
                                     }
-                                } else {
-                                    select_f32_nt_config out = {8u, 4u, 1u, 8u, 8u};
-                                    return out;
                                 }
                             } else {
-                                if (m < INT64_C(278)) {
-                                    select_f32_nt_config out = {8u, 4u, 1u, 8u, 8u};
-                                    return out;
-                                } else {
-                                    if (k < INT64_C(992)) {
-                                        select_f32_nt_config out = {8u, 4u, 1u, 8u, 8u};
+                                if (k < INT64_C(2173)) {
+                                    if (m < INT64_C(29)) {
+                                        select_f32_nt_config out = {4u, 2u, 1u, 8u, 8u};
                                         return out;
                                     } else {
-                                        if (k < INT64_C(2173)) {
-                                            select_f32_nt_config out = {8u, 4u, 4u, 16u, 8u};
+                                        if (m < INT64_C(99)) {
+                                            select_f32_nt_config out = {4u, 1u, 1u, 8u, 8u};
                                             return out;
                                         } else {
-                                            select_f32_nt_config out = {8u, 4u, 1u, 8u, 8u};
+                                            select_f32_nt_config out = {4u, 2u, 1u, 8u, 8u};
                                             return out;
                                         }
                                     }
+                                } else {
+                                    if (m < INT64_C(70)) {
+                                        select_f32_nt_config out = {8u, 1u, 1u, 8u, 8u};
+                                        return out;
+                                    } else {
+                                        if (m < INT64_C(139)) {
+                                            select_f32_nt_config out = {4u, 1u, 1u, 8u, 8u};
+                                            return out;
+                                        } else {
+                                            if (k < INT64_C(3259)) {
+                                                select_f32_nt_config out = {4u, 1u, 1u, 8u, 8u};
+                                                return out;
+                                            } else {
+                                                select_f32_nt_config out = {4u, 2u, 1u, 8u, 8u};
+                                                return out;
+                                            }
+                                        }
+                                    }
+                                }
+                            }
+                        } else {
+                            if (n < INT64_C(544)) {
+                                select_f32_nt_config out = {4u, 2u, 2u, 8u, 8u};
+                                return out;
+                            } else {
+                                if (k < INT64_C(124)) {
+                                    select_f32_nt_config out = {8u, 4u, 4u, 8u, 8u};
+                                    return out;
+                                } else {
+                                    select_f32_nt_config out = {8u, 4u, 4u, 16u, 8u};
+                                    return out;
                                 }
                             }
                         }
                     } else {
-                        if (n < INT64_C(287)) {
-                            if (m < INT64_C(1109)) {
-                                if (k < INT64_C(128)) {
-                                    select_f32_nt_config out = {8u, 4u, 1u, 8u, 8u};
-                                    return out;
-                                } else {
-                                    if (k < INT64_C(725)) {
-                                        select_f32_nt_config out = {8u, 4u, 4u, 16u, 8u};
-                                        return out;
-                                    } else {
-                                        if (k < INT64_C(1536)) {
-                                            select_f32_nt_config out = {4u, 4u, 4u, 8u, 8u};
-                                            return out;
-                                        } else {
-                                            select_f32_nt_config out = {8u, 4u, 1u, 8u, 8u};
-                                            return out;
-                                        }
-                                    }
-                                }
-                            } else {
-                                if (k < INT64_C(128)) {
-                                    select_f32_nt_config out = {4u, 4u, 4u, 8u, 8u};
-                                    return out;
-                                } else {
-                                    if (k < INT64_C(725)) {
-                                        select_f32_nt_config out = {2u, 4u, 4u, 8u, 8u};
-                                        return out;
-                                    } else {
-                                        select_f32_nt_config out = {4u, 4u, 4u, 8u, 8u};
-                                        return out;
-                                    }
-                                }
-                            }
-                        } else {
-                            if (k < INT64_C(256)) {
-                                if (k < INT64_C(79)) {
-                                    select_f32_nt_config out = {4u, 4u, 4u, 8u, 8u};
-                                    return out;
-                                } else {
-                                    select_f32_nt_config out = {8u, 4u, 4u, 16u, 8u};
-                                    return out;
-                                }
-                            } else {
-                                if (m < INT64_C(1109)) {
-                                    select_f32_nt_config out = {4u, 4u, 4u, 8u, 8u};
-                                    return out;
-                                } else {
-                                    select_f32_nt_config out = {2u, 4u, 4u, 8u, 8u};
-                                    return out;
-                                }
-                            }
-                        }
-                    }
-                }
-            } else {
-                if (k < INT64_C(203)) {
-                    select_f32_nt_config out = {2u, 4u, 4u, 8u, 8u};
-                    return out;
-                } else {
-                    if (m < INT64_C(555)) {
-                        if (m < INT64_C(278)) {
+                        if (m < INT64_C(70)) {
                             if (k < INT64_C(405)) {
-                                select_f32_nt_config out = {4u, 4u, 4u, 8u, 8u};
+                                select_f32_nt_config out = {4u, 2u, 1u, 8u, 8u};
                                 return out;
                             } else {
-                                if (n < INT64_C(1449)) {
-                                    select_f32_nt_config out = {8u, 4u, 4u, 16u, 8u};
-                                    return out;
-                                } else {
-                                    select_f32_nt_config out = {4u, 4u, 8u, 16u, 8u};
-                                    return out;
-                                }
+                                select_f32_nt_config out = {4u, 2u, 2u, 8u, 8u};
+                                return out;
                             }
                         } else {
                             if (k < INT64_C(287)) {
-                                select_f32_nt_config out = {2u, 4u, 4u, 8u, 8u};
+                                select_f32_nt_config out = {8u, 4u, 4u, 16u, 8u};
                                 return out;
                             } else {
-                                if (k < INT64_C(573)) {
-                                    select_f32_nt_config out = {8u, 4u, 4u, 16u, 8u};
+                                if (m < INT64_C(139)) {
+                                    if (k < INT64_C(405)) {
+                                        select_f32_nt_config out = {4u, 2u, 2u, 8u, 8u};
+                                        return out;
+                                    } else {
+                                        select_f32_nt_config out = {8u, 4u, 4u, 16u, 8u};
+                                        return out;
+                                    }
+                                } else {
+                                    if (n < INT64_C(1145)) {
+                                        select_f32_nt_config out = {4u, 2u, 2u, 8u, 8u};
+                                        return out;
+                                    } else {
+                                        if (m < INT64_C(278)) {
+                                            select_f32_nt_config out = {8u, 4u, 4u, 8u, 8u};
+                                            return out;
+                                        } else {
+                                            if (k < INT64_C(573)) {
+                                                select_f32_nt_config out = {8u, 4u, 4u, 16u, 8u};
+                                                return out;
+                                            } else {
+                                                select_f32_nt_config out = {8u, 4u, 4u, 8u, 8u};
+                                                return out;
+                                            }
+                                        }
+                                    }
+                                }
+                            }
+                        }
+                    }
+                } else {
+                    if (n < INT64_C(1145)) {
+                        if (n < INT64_C(351)) {
+                            if (m < INT64_C(1109)) {
+                                if (n < INT64_C(287)) {
+                                    select_f32_nt_config out = {4u, 2u, 2u, 8u, 8u};
                                     return out;
                                 } else {
-                                    select_f32_nt_config out = {2u, 4u, 4u, 8u, 8u};
+                                    select_f32_nt_config out = {8u, 4u, 4u, 16u, 8u};
                                     return out;
+                                }
+                            } else {
+                                select_f32_nt_config out = {8u, 4u, 4u, 8u, 8u};
+                                return out;
+                            }
+                        } else {
+                            if (n < INT64_C(992)) {
+                                select_f32_nt_config out = {8u, 4u, 4u, 8u, 8u};
+                                return out;
+                            } else {
+                                if (m < INT64_C(896)) {
+                                    select_f32_nt_config out = {8u, 4u, 4u, 8u, 8u};
+                                    return out;
+                                } else {
+                                    if (m < INT64_C(1268)) {
+                                        select_f32_nt_config out = {8u, 4u, 4u, 16u, 8u};
+                                        return out;
+                                    } else {
+                                        select_f32_nt_config out = {8u, 8u, 4u, 16u, 8u};
+                                        return out;
+                                    }
                                 }
                             }
                         }
                     } else {
-                        if (k < INT64_C(287)) {
-                            if (m < INT64_C(1109)) {
-                                select_f32_nt_config out = {8u, 4u, 4u, 16u, 8u};
-                                return out;
-                            } else {
-                                select_f32_nt_config out = {4u, 4u, 8u, 16u, 8u};
-                                return out;
-                            }
-                        } else {
-                            if (n < INT64_C(1145)) {
-                                if (m < INT64_C(896)) {
-                                    select_f32_nt_config out = {2u, 4u, 4u, 8u, 8u};
-                                    return out;
-                                } else {
-                                    select_f32_nt_config out = {4u, 4u, 8u, 16u, 8u};
-                                    return out;
-                                }
-                            } else {
-                                select_f32_nt_config out = {4u, 4u, 8u, 16u, 8u};
-                                return out;
-                            }
-                        }
+                        select_f32_nt_config out = {8u, 4u, 4u, 16u, 8u};
+                        return out;
                     }
                 }
             }
         }
     } else {
-        if (n < INT64_C(46)) {
-            if (m < INT64_C(8870)) {
-                select_f32_nt_config out = {8u, 4u, 1u, 8u, 8u};
-                return out;
-            } else {
-                if (m < INT64_C(17740)) {
-                    if (k < INT64_C(63)) {
+        if (m < INT64_C(3584)) {
+            if (n < INT64_C(444)) {
+                if (k < INT64_C(46)) {
+                    if (k < INT64_C(28)) {
                         select_f32_nt_config out = {8u, 4u, 4u, 16u, 8u};
                         return out;
                     } else {
-                        if (n < INT64_C(28)) {
-                            select_f32_nt_config out = {8u, 4u, 1u, 8u, 8u};
-                            return out;
-                        } else {
-                            select_f32_nt_config out = {4u, 4u, 4u, 8u, 8u};
-                            return out;
-                        }
+                        select_f32_nt_config out = {8u, 8u, 4u, 16u, 8u};
+                        return out;
                     }
                 } else {
-                    if (n < INT64_C(20)) {
-                        if (m < INT64_C(70960)) {
-                            select_f32_nt_config out = {4u, 4u, 4u, 8u, 8u};
+                    select_f32_nt_config out = {8u, 4u, 4u, 16u, 8u};
+                    return out;
+                }
+            } else {
+                if (k < INT64_C(111)) {
+                    select_f32_nt_config out = {8u, 4u, 4u, 16u, 8u};
+                    return out;
+                } else {
+                    if (k < INT64_C(363)) {
+                        select_f32_nt_config out = {8u, 8u, 4u, 16u, 8u};
+                        return out;
+                    } else {
+                        if (k < INT64_C(1087)) {
+                            select_f32_nt_config out = {8u, 8u, 8u, 16u, 8u};
                             return out;
                         } else {
-                            select_f32_nt_config out = {8u, 4u, 4u, 16u, 8u};
+                            select_f32_nt_config out = {8u, 8u, 4u, 16u, 8u};
                             return out;
                         }
-                    } else {
-                        select_f32_nt_config out = {8u, 4u, 4u, 16u, 8u};
-                        return out;
                     }
                 }
             }
         } else {
-            if (m < INT64_C(3584)) {
-                if (n < INT64_C(314)) {
-                    if (n < INT64_C(222)) {
-                        if (k < INT64_C(46)) {
+            if (k < INT64_C(544)) {
+                if (m < INT64_C(17740)) {
+                    if (n < INT64_C(136)) {
+                        if (k < INT64_C(168)) {
                             select_f32_nt_config out = {8u, 4u, 4u, 16u, 8u};
                             return out;
                         } else {
-                            if (k < INT64_C(222)) {
-                                select_f32_nt_config out = {4u, 4u, 4u, 8u, 8u};
-                                return out;
+                            if (m < INT64_C(8870)) {
+                                if (n < INT64_C(91)) {
+                                    select_f32_nt_config out = {8u, 8u, 4u, 16u, 8u};
+                                    return out;
+                                } else {
+                                    select_f32_nt_config out = {8u, 4u, 4u, 16u, 8u};
+                                    return out;
+                                }
                             } else {
-                                if (k < INT64_C(815)) {
-                                    if (k < INT64_C(314)) {
-                                        select_f32_nt_config out = {2u, 4u, 4u, 8u, 8u};
+                                if (n < INT64_C(91)) {
+                                    if (k < INT64_C(222)) {
+                                        select_f32_nt_config out = {8u, 8u, 4u, 16u, 8u};
                                         return out;
                                     } else {
-                                        if (k < INT64_C(471)) {
-                                            if (n < INT64_C(79)) {
-                                                select_f32_nt_config out = {8u, 4u, 4u, 16u, 8u};
-                                                return out;
-                                            } else {
-                                                select_f32_nt_config out = {2u, 4u, 4u, 8u, 8u};
-                                                return out;
-                                            }
-                                        } else {
-                                            select_f32_nt_config out = {8u, 4u, 4u, 16u, 8u};
-                                            return out;
-                                        }
+                                        select_f32_nt_config out = {8u, 4u, 4u, 16u, 8u};
+                                        return out;
                                     }
                                 } else {
-                                    select_f32_nt_config out = {4u, 4u, 4u, 8u, 8u};
+                                    select_f32_nt_config out = {8u, 8u, 4u, 16u, 8u};
                                     return out;
                                 }
                             }
                         }
                     } else {
-                        select_f32_nt_config out = {2u, 4u, 4u, 8u, 8u};
-                        return out;
-                    }
-                } else {
-                    select_f32_nt_config out = {4u, 4u, 8u, 16u, 8u};
-                    return out;
-                }
-            } else {
-                if (k < INT64_C(20)) {
-                    if (m < INT64_C(50176)) {
-                        select_f32_nt_config out = {2u, 4u, 4u, 8u, 8u};
-                        return out;
-                    } else {
-                        select_f32_nt_config out = {8u, 4u, 4u, 16u, 8u};
-                        return out;
-                    }
-                } else {
-                    if (m < INT64_C(17740)) {
-                        if (n < INT64_C(91)) {
+                        if (k < INT64_C(46)) {
                             if (m < INT64_C(8870)) {
-                                select_f32_nt_config out = {4u, 4u, 4u, 8u, 8u};
+                                select_f32_nt_config out = {8u, 8u, 4u, 16u, 8u};
                                 return out;
                             } else {
-                                if (k < INT64_C(384)) {
+                                select_f32_nt_config out = {8u, 8u, 8u, 16u, 8u};
+                                return out;
+                            }
+                        } else {
+                            select_f32_nt_config out = {8u, 8u, 4u, 16u, 8u};
+                            return out;
+                        }
+                    }
+                } else {
+                    if (k < INT64_C(96)) {
+                        if (m < INT64_C(35480)) {
+                            if (n < INT64_C(46)) {
+                                select_f32_nt_config out = {8u, 4u, 4u, 16u, 8u};
+                                return out;
+                            } else {
+                                select_f32_nt_config out = {8u, 8u, 4u, 16u, 8u};
+                                return out;
+                            }
+                        } else {
+                            select_f32_nt_config out = {8u, 8u, 4u, 16u, 8u};
+                            return out;
+                        }
+                    } else {
+                        if (m < INT64_C(70960)) {
+                            if (k < INT64_C(146)) {
+                                if (m < INT64_C(35480)) {
                                     select_f32_nt_config out = {8u, 4u, 4u, 16u, 8u};
                                     return out;
                                 } else {
-                                    select_f32_nt_config out = {2u, 4u, 4u, 8u, 8u};
+                                    select_f32_nt_config out = {8u, 8u, 4u, 16u, 8u};
+                                    return out;
+                                }
+                            } else {
+                                select_f32_nt_config out = {8u, 8u, 4u, 16u, 8u};
+                                return out;
+                            }
+                        } else {
+                            select_f32_nt_config out = {8u, 8u, 8u, 16u, 8u};
+                            return out;
+                        }
+                    }
+                }
+            } else {
+                if (m < INT64_C(141920)) {
+                    if (n < INT64_C(91)) {
+                        if (m < INT64_C(17740)) {
+                            if (m < INT64_C(8870)) {
+                                select_f32_nt_config out = {8u, 8u, 4u, 16u, 8u};
+                                return out;
+                            } else {
+                                select_f32_nt_config out = {8u, 4u, 4u, 16u, 8u};
+                                return out;
+                            }
+                        } else {
+                            if (m < INT64_C(35480)) {
+                                select_f32_nt_config out = {8u, 8u, 4u, 16u, 8u};
+                                return out;
+                            } else {
+                                if (m < INT64_C(70960)) {
+                                    select_f32_nt_config out = {8u, 8u, 8u, 16u, 8u};
+                                    return out;
+                                } else {
+                                    select_f32_nt_config out = {8u, 8u, 4u, 16u, 8u};
+                                    return out;
+                                }
+                            }
+                        }
+                    } else {
+                        if (m < INT64_C(17740)) {
+                            if (n < INT64_C(182)) {
+                                select_f32_nt_config out = {8u, 8u, 4u, 16u, 8u};
+                                return out;
+                            } else {
+                                if (m < INT64_C(5069)) {
+                                    select_f32_nt_config out = {8u, 8u, 8u, 16u, 8u};
+                                    return out;
+                                } else {
+                                    select_f32_nt_config out = {8u, 8u, 4u, 16u, 8u};
                                     return out;
                                 }
                             }
                         } else {
-                            if (n < INT64_C(222)) {
-                                if (m < INT64_C(8870)) {
-                                    if (k < INT64_C(363)) {
-                                        select_f32_nt_config out = {8u, 4u, 4u, 16u, 8u};
+                            if (m < INT64_C(35480)) {
+                                select_f32_nt_config out = {8u, 8u, 8u, 16u, 8u};
+                                return out;
+                            } else {
+                                if (m < INT64_C(70960)) {
+                                    if (n < INT64_C(182)) {
+                                        select_f32_nt_config out = {8u, 8u, 4u, 16u, 8u};
                                         return out;
                                     } else {
-                                        select_f32_nt_config out = {2u, 4u, 4u, 8u, 8u};
+                                        select_f32_nt_config out = {8u, 8u, 8u, 16u, 8u};
                                         return out;
                                     }
                                 } else {
-                                    select_f32_nt_config out = {4u, 4u, 8u, 16u, 8u};
+                                    select_f32_nt_config out = {8u, 8u, 8u, 16u, 8u};
                                     return out;
                                 }
-                            } else {
-                                select_f32_nt_config out = {4u, 4u, 8u, 16u, 8u};
-                                return out;
                             }
                         }
-                    } else {
-                        select_f32_nt_config out = {4u, 4u, 8u, 16u, 8u};
-                        return out;
                     }
+                } else {
+                    select_f32_nt_config out = {8u, 8u, 8u, 16u, 8u};
+                    return out;
                 }
             }
         }
