@@ -16,6 +16,8 @@ def main():
     ap.add_argument("--family", default="f32")
     ap.add_argument("--trans", default="nn")
     ap.add_argument("--iters", type=int, default=3)
+    ap.add_argument("--schedule", type=int, help="K1 tile schedule (kp_set_schedule)")
+    ap.add_argument("--no-time", action="store_true", help="launch only (sanitizer runs)")
     args = ap.parse_args()
     import torch
     from paper_2003_06795_b200 import gemm
@@ -26,9 +28,15 @@ def main():
     b = torch.rand((n, k) if args.trans[1] == "t" else (k, n), device="cuda").to(dt)
     a = a.t() if args.trans[0] == "t" else a
     b = b.t() if args.trans[1] == "t" else b
+    if args.schedule is not None:
+        from paper_2003_06795_b200 import _native as nat
+        nat.lib().kp_set_schedule(args.schedule)
     for _ in range(args.iters):
         gemm.matmul(a, b, cfg, family=args.family)
     torch.cuda.synchronize()
+    if args.no_time:
+        print(f"{args.family} {args.trans} {(m, k, n)} cfg={cfg}: launched {args.iters}x")
+        return
     ns = gemm.time_config(a, b, cfg, family=args.family, reps=5)
     print(f"{args.family} {args.trans} {(m, k, n)} cfg={cfg}: {ns/1e3:.1f} us, "
           f"{2*m*n*k/ns/1e3:.2f} TFLOP/s")

@@ -3,15 +3,22 @@
 # detection / memcheck). Run on the GPU box:  sh tools/sanitize.sh > gpurun_out/sanitize.log
 set -u
 CS=${CS:-compute-sanitizer}
-run() { echo "== $*"; timeout 300 $CS "$@" 2>&1 | grep -E "ERROR SUMMARY|error|TFLOP" | head -5; }
+run() { echo "== $*"; timeout 300 $CS "$@" 2>&1 | grep -E "ERROR SUMMARY|error|TFLOP|launched" | head -5; }
 for tool in memcheck racecheck; do
   for t in nn nt tn tt; do
-    run --tool $tool python tools/run_config.py --family f32 --trans $t --cfg 8,8,8,16,16 --mkn 17,27,2049 --iters 1
-    run --tool $tool python tools/run_config.py --family f32 --trans $t --cfg 1,1,2,128,1 --mkn 129,15,33 --iters 1
+    run --tool $tool python tools/run_config.py --family f32 --trans $t --cfg 8,8,8,16,16 --mkn 17,27,2049 --iters 1 --no-time
+    run --tool $tool python tools/run_config.py --family f32 --trans $t --cfg 1,1,2,128,1 --mkn 129,15,33 --iters 1 --no-time
   done
+done
+# ordered stream-K hand-off (forced) and the transposed B staging (m >= 2048)
+for tool in memcheck racecheck; do
+  run --tool $tool python tools/run_config.py --family f32 --trans nn --cfg 8,8,8,16,16 --mkn 300,77,200 --schedule 2 --iters 2 --no-time
+  run --tool $tool python tools/run_config.py --family f32 --trans tn --cfg 4,4,4,8,8 --mkn 130,64,70 --schedule 2 --iters 2 --no-time
+  run --tool $tool python tools/run_config.py --family f32 --trans nt --cfg 4,8,8,16,16 --mkn 2053,45,37 --iters 1 --no-time
+  run --tool $tool python tools/run_config.py --family f32 --trans tt --cfg 1,1,2,128,1 --mkn 2053,45,37 --iters 1 --no-time
 done
 for fam in tf32 bf16; do
   for t in nn tt; do
-    run --tool memcheck python tools/run_config.py --family $fam --trans $t --cfg 2,1,2,8,8 --mkn 200,136,264 --iters 1
+    run --tool memcheck python tools/run_config.py --family $fam --trans $t --cfg 2,1,2,8,8 --mkn 200,136,264 --iters 1 --no-time
   done
 done
