@@ -433,8 +433,9 @@ def run_gpu(args) -> int:
                 "h2d_bytes_per_step": sum(2 * 4 * s * s for s in SIZES),
                 "d2h_bytes_per_step": sum(4 * s * s for s in SIZES),
                 "path": "gemm.PinnedPipeline: pinned H2D (copy stream) + kp_gemm_auto "
-                        "(compute stream) + D2H (copy stream), overlapped across the "
-                        "six sizes, synchronised every step"},
+                        "(compute stream) + D2H (copy stream), largest problem first, "
+                        "2048^3 split into 4 row blocks of A/C so its kernels and D2H run "
+                        "under the remaining H2D; synchronised every step"},
         "gpu_launches": launches,
         "clocks": clk,
         "families": families,

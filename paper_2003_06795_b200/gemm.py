@@ -157,10 +157,19 @@ def matmul_pinned(a_host, b_host, out_host, config=None, *, family="f32"):
 
 
 class PinnedPipeline:
-    """End-to-end GEMMs on pinned host buffers with the copies overlapped:
-    H2D of problem i+1 (copy-in stream) runs under the kernel of problem i
-    (compute stream) and the D2H of problem i-1 (copy-out stream); events
-    order the three streams. Device buffers are cached per shape."""
+    """End-to-end GEMMs on pinned host buffers with the copies overlapped.
+
+    Three streams ordered by events: copy-in (H2D), compute, copy-out (D2H).
+    Problems are issued largest first; a large FP32 problem is split into
+    row blocks of A / C (B copied once, first), so the kernel of block j and
+    the D2H of block j-1 run under the H2D of block j+1 and the host link
+    stays busy from the first byte to the last (rows of C are independent
+    and every K1 config accumulates each element in the same k order, so the
+    blocks give exactly the unsplit result).  Device buffers are cached per
+    shape."""
+
+    CHUNK_BYTES = 4 << 20   # A bytes per row block of a split problem
+    MIN_ROWS = 256
 
     def __init__(self, family="f32"):
         torch = _torch()
@@ -181,32 +190,54 @@ class PinnedPipeline:
                                torch.empty(out_host.shape, dtype=torch.float32, device=self.dev))
         return self._bufs[key]
 
+    def _blocks(self, a_host):
+        """Row blocks [(r0, r1)] of one problem (one block unless it is a
+        large 2-D FP32 problem)."""
+        m = a_host.shape[0]
+        if (self.family != "f32" or a_host.dim() != 2 or not a_host.is_contiguous()):
+            return [(0, m)]
+        nbytes = a_host.numel() * a_host.element_size()
+        nblk = min(max(1, -(-nbytes // self.CHUNK_BYTES)), max(1, m // self.MIN_ROWS))
+        step = -(-m // nblk)
+        return [(r, min(m, r + step)) for r in range(0, m, step)]
+
     def run(self, problems, configs=None):
         """problems: [(a_host, b_host, out_host)] pinned; returns when all
         results are in the host buffers."""
         torch = _torch()
-        done_in, done_run = [], []
-        for i, (ha, hb, hc) in enumerate(problems):
-            da, db, dc = self._buffers(i, ha, hb, hc)
-            with torch.cuda.stream(self.s_in):
-                da.copy_(ha, non_blocking=True)
+        order = sorted(range(len(problems)),
+                       key=lambda i: -problems[i][0].numel() * problems[i][1].shape[-1])
+        items = []  # (problem, r0, r1, h2d event)
+        with torch.cuda.stream(self.s_in):
+            for i in order:
+                ha, hb, hc = problems[i]
+                da, db, dc = self._buffers(i, ha, hb, hc)
                 db.copy_(hb, non_blocking=True)
-                ev = torch.cuda.Event()
-                ev.record(self.s_in)
-                done_in.append(ev)
-        for i, (ha, hb, hc) in enumerate(problems):
+                for r0, r1 in self._blocks(ha):
+                    da[r0:r1].copy_(ha[r0:r1], non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(self.s_in)
+                    items.append((i, r0, r1, ev))
+        for i, r0, r1, ev_in in items:
+            ha, hb, hc = problems[i]
             da, db, dc = self._buffers(i, ha, hb, hc)
+            whole = r0 == 0 and r1 == ha.shape[0]
             with torch.cuda.stream(self.s_run):
-                self.s_run.wait_event(done_in[i])
+                self.s_run.wait_event(ev_in)
                 xa, xb = (da, db) if da.dtype == self.want else (da.to(self.want), db.to(self.want))
-                matmul(xa, xb, None if configs is None else configs[i], family=self.family,
-                       out=dc)
+                cfg = None if configs is None else configs[i]
+                if whole:
+                    matmul(xa, xb, cfg, family=self.family, out=dc)
+                else:
+                    matmul(xa[r0:r1], xb, cfg, family=self.family, out=dc[r0:r1])
                 ev = torch.cuda.Event()
                 ev.record(self.s_run)
-                done_run.append(ev)
             with torch.cuda.stream(self.s_out):
                 self.s_out.wait_event(ev)
-                hc.copy_(dc, non_blocking=True)
+                if whole:
+                    hc.copy_(dc, non_blocking=True)
+                else:
+                    hc[r0:r1].copy_(dc[r0:r1], non_blocking=True)
         self.s_out.synchronize()
         return [hc for _, _, hc in problems]
 

@@ -194,11 +194,13 @@ print(json.dumps(out))
 
 def test_pinned_pipeline_matches_device_matmul():
     """The overlapped host-buffer path (bench e2e) returns exactly what the
-    device-resident call returns."""
+    device-resident call returns, also when a large problem is split into row
+    blocks."""
     gemm = _gemm()
     rng = np.random.default_rng(9)
     probs, want = [], []
-    for m, k, n in [(64, 64, 64), (300, 27, 70), (512, 512, 512)]:
+    # (2100, 700, 300): A is 5.9 MB -> split into row blocks (B copied once)
+    for m, k, n in [(64, 64, 64), (300, 27, 70), (512, 512, 512), (2100, 700, 300)]:
         a = torch.from_numpy(rng.uniform(-1, 1, (m, k)).astype(np.float32))
         b = torch.from_numpy(rng.uniform(-1, 1, (k, n)).astype(np.float32))
         probs.append((a.pin_memory(), b.pin_memory(), torch.empty((m, n), pin_memory=True)))
