@@ -663,7 +663,7 @@ kp_status launch(const GemmProblem& g, int wgr, int wgc, cudaStream_t stream) {
     // transposing copy wins +11 % geomean at m >= 4096, breaks even at
     // 1024-4095 and loses 4-9 % below (copy-bound, small m).
     const bool bt = TB && g.m >= 2048;
-    const SmemPlan sp = plan_smem(!TA, TB && !bt, bm, bn);
+    SmemPlan sp = plan_smem(!TA, TB && !bt, bm, bn);
     if (sp.bytes > 227 * 1024) return fail(KP_ERR_UNSUPPORTED, "simt: shared-memory plan too large");
     void (*kern)(const Params) = sp.bk == 32 ? simt_gemm_kernel<ACC, RT, CT, TA, TB, 32, false>
                                              : simt_gemm_kernel<ACC, RT, CT, TA, TB, 16, false>;
@@ -671,11 +671,33 @@ kp_status launch(const GemmProblem& g, int wgr, int wgc, cudaStream_t stream) {
         if (bt) kern = sp.bk == 32 ? simt_gemm_kernel<ACC, RT, CT, TA, TB, 32, true>
                                    : simt_gemm_kernel<ACC, RT, CT, TA, TB, 16, true>;
     }
-    static bool attr_done[2][2] = {{false, false}, {false, false}};  // one process drives one device
-    if (!attr_done[sp.bk == 32][bt]) {
+    static int regs[2][2] = {{0, 0}, {0, 0}};  // one process drives one device
+    if (!regs[sp.bk == 32][bt]) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
             return check_launch("cudaFuncSetAttribute");
-        attr_done[sp.bk == 32][bt] = true;
+        cudaFuncAttributes fa;
+        if (cudaFuncGetAttributes(&fa, kern) != cudaSuccess) return check_launch("cudaFuncGetAttributes");
+        regs[sp.bk == 32][bt] = fa.numRegs > 0 ? fa.numRegs : 128;
+    }
+    // A third cp.async stage only if it does not cost resident CTAs: small
+    // work-groups are register-limited to 4+ CTAs per SM, where 3 stages of
+    // shared memory would cap them at 3 (KP_STAGE_OCC=0: always 3 when they
+    // fit in 112 KB, tuning experiments only).
+    static const bool stage_occ = [] {
+        const char* e = std::getenv("KP_STAGE_OCC");
+        return !(e && e[0] == '0');
+    }();
+    if (stage_occ && sp.stages == 3) {
+        const int nthr = wgr * wgc;
+        const int warp_regs = ((regs[sp.bk == 32][bt] * 32 + 255) / 256) * 256;
+        const int occ_regs = std::min(65536 / (warp_regs * ((nthr + 31) / 32)), 32);
+        const size_t smem_sm = 228 * 1024, stage_bytes = sp.bytes / 3;
+        const int occ3 = std::min<int>(occ_regs, int(smem_sm / (3 * stage_bytes + 1024)));
+        const int occ2 = std::min<int>(occ_regs, int(smem_sm / (2 * stage_bytes + 1024)));
+        if (occ2 > occ3) {
+            sp.stages = 2;
+            sp.bytes = 2 * stage_bytes;
+        }
     }
     Params p;
     p.A = static_cast<const float*>(g.A);

@@ -1,4 +1,3 @@
-for spec in "1,1,4,8,8" "4,2,8,16,16" "4,1,8,16,16"; do
-  timeout 300 ncu --set full --clock-control none -k regex:tc_gemm -s 2 -c 1 -o gpurun_out/prof_bf16_2048_${spec//,/} python tools/run_config.py --family bf16 --mkn 2048,2048,2048 --cfg $spec --iters 3 > gpurun_out/ncu_tc.log 2>&1
-  python tools/run_config.py --family bf16 --mkn 2048,2048,2048 --cfg $spec --iters 3
-done
+CF="1,8,8,32,8;2,8,4,16,8;4,8,4,16,16;4,8,8,32,8;8,8,4,16,8;8,8,4,16,16;4,4,4,16,8;2,4,4,16,8;4,2,2,8,8;8,8,2,8,16"
+KP_STAGE_OCC=0 timeout 900 python tools/k1_ab.py --tag old --sizes 512,1024,2048,4096 --cfgs "$CF" > gpurun_out/ab_st_old.jsonl 2>&1
+timeout 900 python tools/k1_ab.py --tag new --sizes 512,1024,2048,4096 --cfgs "$CF" > gpurun_out/ab_st_new.jsonl 2>&1
