@@ -1,0 +1,352 @@
+#ifndef SELECT_F32_TN_H
+#define SELECT_F32_TN_H
+
+#include <stdint.h>
+
+typedef struct {
+    uint32_t acc;
+    uint32_t row_tile;
+    uint32_t col_tile;
+    uint32_t wg_rows;
+    uint32_t wg_cols;
+} select_f32_tn_config;
+
+static inline select_f32_tn_config select_f32_tn(int64_t m, int64_t k, int64_t n) {
+    (void)m;
+    (void)k;
+    (void)n;
+    if (m < INT64_C(3584)) {
+        if (m < INT64_C(159)) {
+            if (n < INT64_C(1132)) {
+                if (m < INT64_C(29)) {
+                    select_f32_tn_config out = {2u, 1u, 1u, 8u, 8u};
+                    return out;
+                } else {
+                    if (n < INT64_C(405)) {
+                        select_f32_tn_config out = {2u, 1u, 1u, 8u, 8u};
+                        return out;
+                    } else {
+                        if (k < INT64_C(1449)) {
+                            select_f32_tn_config out = {8u, 2u, 2u, 8u, 8u};
+                            return out;
+                        } else {
+                            if (m < INT64_C(70)) {
+                                select_f32_tn_config out = {2u, 1u, 1u, 8u, 8u};
+                                return out;
+                            } else {
+                                select_f32_tn_config out = {8u, 2u, 2u, 8u, 8u};
+                                return out;
+                            }
+                        }
+                    }
+                }
+            } else {
+                if (m < INT64_C(12)) {
+                    if (m < INT64_C(6)) {
+                        if (m < INT64_C(2)) {
+                            select_f32_tn_config out = {2u, 1u, 1u, 8u, 8u};
+                            return out;
+                        } else {
+                            select_f32_tn_config out = {8u, 2u, 2u, 8u, 8u};
+                            return out;
+                        }
+                    } else {
+                        select_f32_tn_config out = {2u, 1u, 1u, 8u, 8u};
+                        return out;
+                    }
+                } else {
+                    if (m < INT64_C(70)) {
+                        select_f32_tn_config out = {8u, 2u, 2u, 8u, 8u};
+                        return out;
+                    } else {
+                        if (k < INT64_C(405)) {
+                            select_f32_tn_config out = {8u, 2u, 2u, 8u, 8u};
+                            return out;
+                        } else {
+                            select_f32_tn_config out = {8u, 4u, 4u, 8u, 8u};
+                            return out;
+                        }
+                    }
+                }
+            }
+        } else {
+            if (n < INT64_C(351)) {
+                if (m < INT64_C(555)) {
+                    if (n < INT64_C(124)) {
+                        select_f32_tn_config out = {2u, 1u, 1u, 8u, 8u};
+                        return out;
+                    } else {
+                        if (n < INT64_C(287)) {
+                            if (n < INT64_C(203)) {
+                                if (m < INT64_C(278)) {
+                                    if (k < INT64_C(744)) {
+                                        select_f32_tn_config out = {2u, 1u, 1u, 8u, 8u};
+                                        return out;
+                                    } else {
+                                        select_f32_tn_config out = {8u, 2u, 2u, 8u, 8u};
+                                        return out;
+                                    }
+                                } else {
+                                    select_f32_tn_config out = {8u, 2u, 2u, 8u, 8u};
+                                    return out;
+                                }
+                            } else {
+                                select_f32_tn_config out = {8u, 2u, 2u, 8u, 8u};
+                                return out;
+                            }
+                        } else {
+                            select_f32_tn_config out = {8u, 4u, 4u, 8u, 8u};
+                            return out;
+                        }
+                    }
+                } else {
+                    if (n < INT64_C(136)) {
+                        if (m < INT64_C(1109)) {
+                            select_f32_tn_config out = {8u, 2u, 2u, 8u, 8u};
+                            return out;
+                        } else {
+                            if (n < INT64_C(111)) {
+                                if (m < INT64_C(2218)) {
+                                    if (n < INT64_C(46)) {
+                                        select_f32_tn_config out = {8u, 2u, 2u, 8u, 8u};
+                                        return out;
+                                    } else {
+                                        if (n < INT64_C(79)) {
+                                            if (k < INT64_C(272)) {
+                                                select_f32_tn_config out = {8u, 4u, 4u, 8u, 8u};
+                                                return out;
+                                            } else {
+                                                select_f32_tn_config out = {8u, 2u, 2u, 8u, 8u};
+                                                return out;
+                                            }
+                                        } else {
+                                            select_f32_tn_config out = {8u, 4u, 4u, 8u, 8u};
+                                            return out;
+                                        }
+                                    }
+                                } else {
+                                    select_f32_tn_config out = {8u, 4u, 4u, 8u, 8u};
+                                    return out;
+                                }
+                            } else {
+                                if (m < INT64_C(2218)) {
+                                    select_f32_tn_config out = {8u, 4u, 4u, 8u, 8u};
+                                    return out;
+                                } else {
+                                    select_f32_tn_config out = {8u, 8u, 4u, 8u, 16u};
+                                    return out;
+                                }
+                            }
+                        }
+                    } else {
+                        if (m < INT64_C(2218)) {
+                            if (m < INT64_C(1109)) {
+                                select_f32_tn_config out = {8u, 4u, 4u, 8u, 8u};
+                                return out;
+                            } else {
+                                if (k < INT64_C(128)) {
+                                    select_f32_tn_config out = {8u, 4u, 4u, 8u, 8u};
+                                    return out;
+                                } else {
+                                    if (k < INT64_C(725)) {
+                                        select_f32_tn_config out = {8u, 8u, 4u, 8u, 16u};
+                                        return out;
+                                    } else {
+                                        select_f32_tn_config out = {8u, 4u, 4u, 8u, 8u};
+                                        return out;
+                                    }
+                                }
+                            }
+                        } else {
+                            if (k < INT64_C(128)) {
+                                if (k < INT64_C(28)) {
+                                    select_f32_tn_config out = {8u, 4u, 4u, 8u, 8u};
+                                    return out;
+                                } else {
+                                    select_f32_tn_config out = {8u, 8u, 4u, 16u, 8u};
+                                    return out;
+                                }
+                            } else {
+                                select_f32_tn_config out = {4u, 8u, 8u, 16u, 8u};
+                                return out;
+                            }
+                        }
+                    }
+                }
+            } else {
+                if (m < INT64_C(634)) {
+                    if (n < INT64_C(744)) {
+                        if (m < INT64_C(278)) {
+                            if (k < INT64_C(314)) {
+                                select_f32_tn_config out = {8u, 4u, 4u, 8u, 8u};
+                                return out;
+                            } else {
+                                select_f32_tn_config out = {8u, 2u, 2u, 8u, 8u};
+                                return out;
+                            }
+                        } else {
+                            select_f32_tn_config out = {8u, 4u, 4u, 8u, 8u};
+                            return out;
+                        }
+                    } else {
+                        if (m < INT64_C(278)) {
+                            if (n < INT64_C(1620)) {
+                                select_f32_tn_config out = {8u, 4u, 4u, 8u, 8u};
+                                return out;
+                            } else {
+                                select_f32_tn_config out = {8u, 8u, 4u, 8u, 16u};
+                                return out;
+                            }
+                        } else {
+                            if (k < INT64_C(573)) {
+                                select_f32_tn_config out = {8u, 8u, 4u, 8u, 16u};
+                                return out;
+                            } else {
+                                select_f32_tn_config out = {4u, 8u, 8u, 16u, 8u};
+                                return out;
+                            }
+                        }
+                    }
+                } else {
+                    if (n < INT64_C(992)) {
+                        if (m < INT64_C(1109)) {
+                            select_f32_tn_config out = {8u, 8u, 4u, 8u, 16u};
+                            return out;
+                        } else {
+                            if (m < INT64_C(2218)) {
+                                if (k < INT64_C(544)) {
+                                    if (n < INT64_C(544)) {
+                                        select_f32_tn_config out = {8u, 8u, 4u, 8u, 16u};
+                                        return out;
+                                    } else {
+                                        select_f32_tn_config out = {8u, 8u, 4u, 16u, 8u};
+                                        return out;
+                                    }
+                                } else {
+                                    select_f32_tn_config out = {4u, 8u, 8u, 16u, 8u};
+                                    return out;
+                                }
+                            } else {
+                                select_f32_tn_config out = {8u, 8u, 4u, 8u, 16u};
+                                return out;
+                            }
+                        }
+                    } else {
+                        if (n < INT64_C(1145)) {
+                            if (m < INT64_C(1268)) {
+                                select_f32_tn_config out = {4u, 8u, 8u, 16u, 8u};
+                                return out;
+                            } else {
+                                if (m < INT64_C(2218)) {
+                                    select_f32_tn_config out = {8u, 8u, 4u, 8u, 16u};
+                                    return out;
+                                } else {
+                                    select_f32_tn_config out = {4u, 8u, 8u, 16u, 8u};
+                                    return out;
+                                }
+                            }
+                        } else {
+                            select_f32_tn_config out = {8u, 8u, 4u, 8u, 16u};
+                            return out;
+                        }
+                    }
+                }
+            }
+        }
+    } else {
+        if (k < INT64_C(46)) {
+            if (m < INT64_C(8870)) {
+                select_f32_tn_config out = {8u, 8u, 4u, 8u, 16u};
+                return out;
+            } else {
+                if (m < INT64_C(401409)) {
+                    if (m < INT64_C(17740)) {
+                        if (k < INT64_C(26)) {
+                            select_f32_tn_config out = {4u, 8u, 8u, 16u, 8u};
+                            return out;
+                        } else {
+                            select_f32_tn_config out = {8u, 8u, 4u, 16u, 8u};
+                            return out;
+                        }
+                    } else {
+                        select_f32_tn_config out = {8u, 8u, 4u, 16u, 8u};
+                        return out;
+                    }
+                } else {
+                    select_f32_tn_config out = {4u, 8u, 8u, 16u, 8u};
+                    return out;
+                }
+            }
+        } else {
+            if (n < INT64_C(46)) {
+                if (m < INT64_C(8870)) {
+                    select_f32_tn_config out = {8u, 4u, 4u, 8u, 8u};
+                    return out;
+                } else {
+                    select_f32_tn_config out = {8u, 8u, 4u, 16u, 8u};
+                    return out;
+                }
+            } else {
+                if (m < INT64_C(35480)) {
+                    if (n < INT64_C(363)) {
+                        if (m < INT64_C(17740)) {
+                            if (m < INT64_C(8870)) {
+                                if (k < INT64_C(544)) {
+                                    if (k < INT64_C(128)) {
+                                        select_f32_tn_config out = {8u, 8u, 4u, 8u, 16u};
+                                        return out;
+                                    } else {
+                                        if (n < INT64_C(91)) {
+                                            select_f32_tn_config out = {8u, 8u, 4u, 8u, 16u};
+                                            return out;
+                                        } else {
+                                            select_f32_tn_config out = {4u, 8u, 8u, 16u, 8u};
+                                            return out;
+                                        }
+                                    }
+                                } else {
+                                    select_f32_tn_config out = {8u, 8u, 4u, 8u, 16u};
+                                    return out;
+                                }
+                            } else {
+                                if (n < INT64_C(91)) {
+                                    select_f32_tn_config out = {4u, 8u, 8u, 16u, 8u};
+                                    return out;
+                                } else {
+                                    if (n < INT64_C(182)) {
+                                        select_f32_tn_config out = {8u, 8u, 4u, 8u, 16u};
+                                        return out;
+                                    } else {
+                                        select_f32_tn_config out = {4u, 8u, 8u, 16u, 8u};
+                                        return out;
+                                    }
+                                }
+                            }
+                        } else {
+                            if (n < INT64_C(91)) {
+                                if (k < INT64_C(384)) {
+                                    select_f32_tn_config out = {8u, 8u, 4u, 16u, 8u};
+                                    return out;
+                                } else {
+                                    select_f32_tn_config out = {8u, 8u, 4u, 8u, 16u};
+                                    return out;
+                                }
+                            } else {
+                                select_f32_tn_config out = {4u, 8u, 8u, 16u, 8u};
+                                return out;
+                            }
+                        }
+                    } else {
+                        select_f32_tn_config out = {4u, 8u, 8u, 16u, 8u};
+                        return out;
+                    }
+                } else {
+                    select_f32_tn_config out = {4u, 8u, 8u, 16u, 8u};
+                    return out;
+                }
+            }
+        }
+    }
+}
+
+#endif /* SELECT_F32_TN_H */

@@ -314,3 +314,19 @@ def test_every_config_bit_exact_tall_b_transposed(ta):
         if not np.array_equal(got, want):
             bad.append(cfg.as_tuple())
     assert not bad, f"{len(bad)} configs differ, first {bad[:5]}"
+
+
+@pytest.mark.parametrize("ta,tb", [(False, False), (False, True), (True, False), (True, True)])
+def test_runtime_selection_every_layout(ta, tb):
+    """kp_gemm_auto has a compiled selector for every FP32 operand layout
+    (the sweep + prune + decision-tree pipeline ran per layout) and the
+    selected kernel is bit-exact vs the oracle."""
+    gemm = _gemm()
+    for (m, k, n) in [(17, 27, 15), (200, 576, 64), (2100, 64, 96)]:
+        rng = np.random.default_rng(m + 3 * k + 7 * n)
+        a_store, b_store, a, b = _operands(rng, m, k, n, ta, tb)
+        cfg = gemm.select(m, k, n, trans_a=ta, trans_b=tb)
+        got = gemm.matmul(a, b).cpu().numpy()
+        want = gemm_f32_exact(a_store, b_store, m=m, k=k, n=n, trans_a=ta,
+                              trans_b=tb).reshape(m, n)
+        np.testing.assert_array_equal(got, want, err_msg=f"{(m, k, n)} {cfg}")

@@ -1,3 +1,6 @@
-CF="1,8,8,32,8;2,8,4,16,8;4,8,4,16,16;4,8,8,32,8;8,8,4,16,8;8,8,4,16,16;4,4,4,16,8;2,4,4,16,8;4,2,2,8,8;8,8,2,8,16"
-KP_STAGE_OCC=0 timeout 900 python tools/k1_ab.py --tag old --sizes 512,1024,2048,4096 --cfgs "$CF" > gpurun_out/ab_st_old.jsonl 2>&1
-timeout 900 python tools/k1_ab.py --tag new --sizes 512,1024,2048,4096 --cfgs "$CF" > gpurun_out/ab_st_new.jsonl 2>&1
+set -x
+timeout 1200 python -m pytest tests/ -x -q -m gpu 2>&1 | tail -3
+for t in nn nt tn tt; do
+  timeout 1500 python -m paper_2003_06795_b200 sweep --shapes networks+squares --family f32 --trans $t --out gpurun_out/b200_f32_${t}_train.csv --sidecar gpurun_out/b200_f32_${t}_train.sidecar.json > gpurun_out/sweep_$t.log 2>&1
+  tail -1 gpurun_out/sweep_$t.log
+done
