@@ -1,6 +1,2 @@
-set -x
-timeout 1200 python -m pytest tests/ -x -q -m gpu 2>&1 | tail -3
-for t in nn nt tn tt; do
-  timeout 1500 python -m paper_2003_06795_b200 sweep --shapes networks+squares --family f32 --trans $t --out gpurun_out/b200_f32_${t}_train.csv --sidecar gpurun_out/b200_f32_${t}_train.sidecar.json > gpurun_out/sweep_$t.log 2>&1
-  tail -1 gpurun_out/sweep_$t.log
-done
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:simt_gemm -s 2 -c 1 -o gpurun_out/prof_sel2_2048 python tools/run_config.py --mkn 2048,2048,2048 --cfg 2,4,8,16,8 --iters 3 > gpurun_out/ncu_sel.log 2>&1
+tail -1 gpurun_out/ncu_sel.log
