@@ -730,7 +730,14 @@ kp_status launch(const GemmProblem& g, int wgr, int wgc, cudaStream_t stream) {
     // of the last wave idle.  beta == 0 only (C doubles as the hand-off
     // buffer); at least one k-slice range per CTA, so a tile is split between
     // at most two CTAs and no CTA waits on a chain.
-    const int sched = simt_schedule();
+    int sched = simt_schedule();
+    // A CUDA-graph capture would bake one flag epoch into every replay (the
+    // waiter would see its own epoch from the previous replay): captured
+    // launches always take one tile per CTA.
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (sched != 0 && cudaStreamIsCapturing(stream, &cap) == cudaSuccess &&
+        cap != cudaStreamCaptureStatusNone)
+        sched = 0;
     const int64_t T = tiles * g.batch;
     const int64_t KT = (g.k + sp.bk - 1) / sp.bk;
     if (sched != 0 && g.beta == 0.0f && T >= 2 && KT >= 2 && T * KT < (int64_t(1) << 40)) {

@@ -166,14 +166,21 @@ class PinnedPipeline:
     stays busy from the first byte to the last (rows of C are independent
     and every K1 config accumulates each element in the same k order, so the
     blocks give exactly the unsplit result).  Device buffers are cached per
-    shape."""
+    shape.
 
-    CHUNK_BYTES = 4 << 20   # A bytes per row block of a split problem
+    ``graph=True`` captures one step per distinct problem list (same host
+    buffers) into a CUDA graph on first use and replays it afterwards: the
+    whole H2D / kernel / D2H schedule then costs one launch of host work.
+    Replays read whatever the host buffers hold at replay time."""
+
+    CHUNK_BYTES = 4 << 20   # A bytes per row block of a split problem (tools/e2e_probe.py)
     MIN_ROWS = 256
 
-    def __init__(self, family="f32"):
+    def __init__(self, family="f32", graph: bool = False):
         torch = _torch()
         self.family = family
+        self.graph = graph
+        self._graphs = {}
         self.want = _family_dtype(nat.family_id(family))
         self.dev = torch.device("cuda", torch.cuda.current_device())
         self.s_in = torch.cuda.Stream(self.dev)
@@ -204,6 +211,33 @@ class PinnedPipeline:
     def run(self, problems, configs=None):
         """problems: [(a_host, b_host, out_host)] pinned; returns when all
         results are in the host buffers."""
+        torch = _torch()
+        if not self.graph:
+            self._enqueue(problems, configs)
+            self.s_out.synchronize()
+            return [hc for _, _, hc in problems]
+        key = tuple((a.data_ptr(), b.data_ptr(), c.data_ptr(), tuple(a.shape), tuple(b.shape),
+                     tuple(c.shape)) for a, b, c in problems)
+        key += (None if configs is None else tuple(tuple(_cfg_tuple(c)) for c in configs),)
+        entry = self._graphs.get(key)
+        if entry is None:
+            self._enqueue(problems, configs)   # buffers, selectors, kernel attributes
+            self.s_out.synchronize()
+            g = torch.cuda.CUDAGraph()
+            cap = torch.cuda.Stream(self.dev)
+            cap.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.graph(g, stream=cap):
+                for st in (self.s_in, self.s_run, self.s_out):
+                    st.wait_stream(cap)
+                self._enqueue(problems, configs)
+                for st in (self.s_in, self.s_run, self.s_out):
+                    cap.wait_stream(st)
+            entry = self._graphs[key] = g
+        entry.replay()
+        torch.cuda.current_stream().synchronize()
+        return [hc for _, _, hc in problems]
+
+    def _enqueue(self, problems, configs):
         torch = _torch()
         order = sorted(range(len(problems)),
                        key=lambda i: -problems[i][0].numel() * problems[i][1].shape[-1])
@@ -238,8 +272,10 @@ class PinnedPipeline:
                     hc.copy_(dc, non_blocking=True)
                 else:
                     hc[r0:r1].copy_(dc[r0:r1], non_blocking=True)
-        self.s_out.synchronize()
-        return [hc for _, _, hc in problems]
+
+
+def _cfg_tuple(cfg):
+    return cfg.as_tuple() if hasattr(cfg, "as_tuple") else tuple(cfg)
 
 
 def time_config(a, b, config, *, family="f32", out=None, warmup: int = 3, reps: int = 10,

@@ -212,6 +212,25 @@ def test_pinned_pipeline_matches_device_matmul():
             assert torch.equal(g, w)
 
 
+def test_pinned_pipeline_graph_replays_track_host_data():
+    """graph=True captures the step once; replays read the host buffers'
+    current contents (new data in the same pinned buffers -> new results)."""
+    gemm = _gemm()
+    rng = np.random.default_rng(10)
+    shapes = [(64, 64, 64), (300, 27, 70), (2100, 700, 300)]
+    probs = [(torch.empty((m, k)).pin_memory(), torch.empty((k, n)).pin_memory(),
+              torch.empty((m, n), pin_memory=True)) for m, k, n in shapes]
+    pipe = gemm.PinnedPipeline("f32", graph=True)
+    for _ in range(3):
+        for (m, k, n), (ha, hb, _) in zip(shapes, probs):
+            ha.copy_(torch.from_numpy(rng.uniform(-1, 1, (m, k)).astype(np.float32)))
+            hb.copy_(torch.from_numpy(rng.uniform(-1, 1, (k, n)).astype(np.float32)))
+        got = pipe.run(probs)
+        for (ha, hb, _), g in zip(probs, got):
+            assert torch.equal(g, gemm.matmul(ha.cuda(), hb.cuda()).cpu())
+    assert len(pipe._graphs) == 1
+
+
 @pytest.fixture
 def schedule():
     """Set the K1 tile-scheduling mode (kp_set_schedule) for one test."""
