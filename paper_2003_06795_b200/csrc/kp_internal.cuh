@@ -48,6 +48,11 @@ kp_status sk_reserve(uint32_t n, SkFlags* out);
 int simt_schedule();
 // Number of SMs of the current device (cached).
 int sm_count();
+// The calling thread's current CUDA device (0 if the query fails).
+inline int current_device() {
+    int dev = 0;
+    return cudaGetDevice(&dev) == cudaSuccess ? dev : 0;
+}
 
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 

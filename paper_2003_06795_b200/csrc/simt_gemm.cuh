@@ -35,6 +35,7 @@
 #pragma once
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <map>
 #include <type_traits>
@@ -671,13 +672,17 @@ kp_status launch(const GemmProblem& g, int wgr, int wgc, cudaStream_t stream) {
         if (bt) kern = sp.bk == 32 ? simt_gemm_kernel<ACC, RT, CT, TA, TB, 32, true>
                                    : simt_gemm_kernel<ACC, RT, CT, TA, TB, 16, true>;
     }
-    static int regs[2][2] = {{0, 0}, {0, 0}};  // one process drives one device
-    if (!regs[sp.bk == 32][bt]) {
+    // per-device opt-in to > 48 KB of dynamic shared memory, register count per kernel
+    static std::atomic<uint64_t> attr_set[2][2] = {};
+    static int regs[2][2] = {{0, 0}, {0, 0}};
+    const uint64_t dev_bit = uint64_t(1) << (current_device() & 63);
+    if (!(attr_set[sp.bk == 32][bt].load(std::memory_order_acquire) & dev_bit)) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
             return check_launch("cudaFuncSetAttribute");
         cudaFuncAttributes fa;
         if (cudaFuncGetAttributes(&fa, kern) != cudaSuccess) return check_launch("cudaFuncGetAttributes");
         regs[sp.bk == 32][bt] = fa.numRegs > 0 ? fa.numRegs : 128;
+        attr_set[sp.bk == 32][bt].fetch_or(dev_bit, std::memory_order_release);
     }
     // A third cp.async stage only if it does not cost resident CTAs: small
     // work-groups are register-limited to 4+ CTAs per SM, where 3 stages of

@@ -30,6 +30,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <mutex>
 
@@ -726,11 +727,12 @@ static kp_status launch_t(const GemmProblem& g, int want_stages, cudaStream_t st
     else       st = make_map(&mb, bf16, g.B, g.n, g.k, bat_b, g.ldb, g.sb, MB::ATOM, BK, MB::TMA_SWIZZLE);
     if (st != KP_OK) return st;
     auto kern = tc_gemm_kernel<ES, BN, A_MN, B_MN, NBUF>;
-    static bool attr_done = false;
-    if (!attr_done) {
+    static std::atomic<uint64_t> attr_set{0};  // per-device opt-in to > 48 KB dynamic smem
+    const uint64_t dev_bit = uint64_t(1) << (current_device() & 63);
+    if (!(attr_set.load(std::memory_order_acquire) & dev_bit)) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
             return check_launch("cudaFuncSetAttribute");
-        attr_done = true;
+        attr_set.fetch_or(dev_bit, std::memory_order_release);
     }
     TcParams p;
     p.C = g.C;
@@ -778,11 +780,12 @@ static kp_status launch_pair(const GemmProblem& g, int want_stages, cudaStream_t
     else       st = make_map(&mb, bf16, g.B, g.n, g.k, bat_b, g.ldb, g.sb, MB::ATOM, BK, MB::TMA_SWIZZLE);
     if (st != KP_OK) return st;
     auto kern = tc_gemm_pair_kernel<ES, BN, A_MN, B_MN>;
-    static bool attr_done = false;
-    if (!attr_done) {
+    static std::atomic<uint64_t> attr_set{0};  // per-device opt-in to > 48 KB dynamic smem
+    const uint64_t dev_bit = uint64_t(1) << (current_device() & 63);
+    if (!(attr_set.load(std::memory_order_acquire) & dev_bit)) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
             return check_launch("cudaFuncSetAttribute");
-        attr_done = true;
+        attr_set.fetch_or(dev_bit, std::memory_order_release);
     }
     TcParams p;
     p.C = g.C;

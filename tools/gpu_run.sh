@@ -1,2 +1,4 @@
-timeout 900 python tools/net_bench.py --batch 8 --out gpurun_out/net_bench.json > gpurun_out/net_bench.log 2>&1; tail -2 gpurun_out/net_bench.log
-KP_BENCH_SHARE_DEVICE=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --steps 50 --warmup 3 > gpurun_out/bench_w2.json 2> gpurun_out/bench_w2.err; tail -2 gpurun_out/bench_w2.err
+set -x
+timeout 1200 python -m pytest tests/ -x -q -m gpu 2>&1 | tail -3
+python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -2 gpurun_out/bench.err
