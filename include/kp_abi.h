@@ -97,13 +97,13 @@ kp_status kp_config_valid(kp_family family, kp_config cfg);
 kp_status kp_gemm(kp_family family, kp_config cfg, const kp_gemm_desc* desc,
                   const void* A, const void* B, float* C, void* stream);
 
-/* Timing loop (K4).  One untimed launch, one timed launch that sizes the
- * samples, `warmup`-1 more untimed launches, then `reps` samples of
- * back-to-back launches (each sample >= min_sample_ns of device time);
+/* Timing loop (K4).  One timed launch that sizes the samples (it also
+ * absorbs first-launch costs), `warmup`-1 more untimed launches, then `reps`
+ * samples of back-to-back launches (each sample >= min_sample_ns of device time);
  * *runtime_ns = median per-launch device time (CUDA events on `stream`).
  * Cell budget: when reps * (one launch) exceeds max_cell_ns (> 0), the extra
  * warm-ups are skipped and reps shrinks to fit (at least 1 sample), so
- * hopeless configs on big problems cost ~3 launches.  Synchronises `stream`. */
+ * hopeless configs on big problems cost ~2 launches.  Synchronises `stream`. */
 kp_status kp_gemm_time(kp_family family, kp_config cfg, const kp_gemm_desc* desc,
                        const void* A, const void* B, float* C,
                        int32_t warmup, int32_t reps, double min_sample_ns,

@@ -201,8 +201,8 @@ static kp_status time_one(kp_family fam, const kp_config& c, const GemmProblem& 
     kp_status st;
     if ((st = g_events.ensure(2 * size_t(reps) + 2)) != KP_OK) return st;
     cudaEvent_t* ev = g_events.ev.data();
-    // first (cold) launch, then one timed launch to size the samples
-    if ((st = run(fam, c, g, s)) != KP_OK) return st;
+    // one timed launch sizes the samples and doubles as the cold launch (its
+    // first-launch costs only make the sizing conservative)
     cudaEventRecord(ev[0], s);
     if ((st = run(fam, c, g, s)) != KP_OK) return st;
     cudaEventRecord(ev[1], s);

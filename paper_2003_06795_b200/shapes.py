@@ -95,6 +95,11 @@ PROBLEM_SETS = {
     "networks+squares": lambda: tuple(dict.fromkeys(
         network_problems(batches=(1, 2, 4, 8, 16))
         + square_problems((64, 128, 256, 512, 1024, 2048, 4096)))),
+    # generalisation check: the batch-32/64 network shapes the selectors were
+    # never trained on (BASELINE configs[2] spans batch 1-64)
+    "networks-unseen": lambda: tuple(
+        p for p in network_problems(batches=(32, 64))
+        if p not in set(PROBLEM_SETS["networks+squares"]())),
 }
 
 
