@@ -426,7 +426,9 @@ def run_gpu(args) -> int:
         "pct_oracle_best": pct_best,
         "sweep": {"cells": len(f32.cells), "wall_s": f32.sweep_wall,
                   "cells_per_s": len(f32.cells) / f32.sweep_wall if f32.cells else None,
-                  "timing": "warm L2, median of reps, C++ loop (kp_sweep_problem)"},
+                  "timing": "warm L2, median of reps, C++ loop (kp_sweep_problem); a "
+                            "config > 1 ms and > 8x the size's best so far keeps its first "
+                            "timing"},
         "per_size": per_size,
         "roofline": roofline,
         "e2e": {"value": e2e_value, "unit": "TFLOP/s",

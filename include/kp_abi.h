@@ -110,7 +110,9 @@ kp_status kp_gemm_time(kp_family family, kp_config cfg, const kp_gemm_desc* desc
                        double max_cell_ns, double* runtime_ns, void* stream);
 
 /* Time every config in `cfgs` on one problem (buffers allocated once by the
- * caller); runtime_ns[i] per config, same timing method as kp_gemm_time. */
+ * caller); runtime_ns[i] per config, same timing method as kp_gemm_time,
+ * except that a config whose first launch takes over 1 ms and over 8x the
+ * best median of this problem so far keeps that single timing. */
 kp_status kp_sweep_problem(kp_family family, const kp_config* cfgs, int32_t n_cfgs,
                            const kp_gemm_desc* desc, const void* A, const void* B,
                            float* C, int32_t warmup, int32_t reps,

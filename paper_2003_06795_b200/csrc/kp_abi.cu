@@ -196,7 +196,7 @@ static thread_local EventPool g_events;
 
 static kp_status time_one(kp_family fam, const kp_config& c, const GemmProblem& g, int warmup,
                           int reps, double min_sample_ns, double max_cell_ns, double* out,
-                          cudaStream_t s) {
+                          cudaStream_t s, double hopeless_ns = 0.0) {
     if (reps < 1) return fail(KP_ERR_INVALID_ARG, "reps must be >= 1");
     kp_status st;
     if ((st = g_events.ensure(2 * size_t(reps) + 2)) != KP_OK) return st;
@@ -210,6 +210,10 @@ static kp_status time_one(kp_family fam, const kp_config& c, const GemmProblem& 
     float one_ms = 0.f;
     cudaEventElapsedTime(&one_ms, ev[0], ev[1]);
     const double one_ns = std::max(1.0, double(one_ms) * 1e6);
+    if (hopeless_ns > 0.0 && one_ns > hopeless_ns) {  // sweep: far off the best so far
+        *out = one_ns;
+        return KP_OK;
+    }
     int nreps = reps;
     bool budget_hit = false;
     if (max_cell_ns > 0.0 && one_ns * reps > max_cell_ns) {
@@ -306,9 +310,15 @@ kp_status kp_sweep_problem(kp_family family, const kp_config* cfgs, int32_t n_cf
     if ((st = to_problem(desc, A, B, C, &g)) != KP_OK) return st;
     for (int32_t i = 0; i < n_cfgs; ++i)
         if ((st = valid_config(family, cfgs[i])) != KP_OK) return st;
+    // A config whose first launch is both over 1 ms and 8x the best median of
+    // this problem so far keeps that single timing: it normalises below
+    // 0.125 either way and the extra launches would dominate the sweep.
+    double best = 0.0;
     for (int32_t i = 0; i < n_cfgs; ++i) {
+        const double hopeless = best > 0.0 ? std::max(1e6, 8.0 * best) : 0.0;
         st = time_one(family, cfgs[i], g, warmup, reps, min_sample_ns, max_cell_ns,
-                      runtime_ns + i, static_cast<cudaStream_t>(stream));
+                      runtime_ns + i, static_cast<cudaStream_t>(stream), hopeless);
+        if (st == KP_OK && (best == 0.0 || runtime_ns[i] < best)) best = runtime_ns[i];
         if (st != KP_OK) {
             char buf[96];
             snprintf(buf, sizeof buf, " [config #%d (%u,%u,%u,%u,%u)]", i, cfgs[i].acc,
