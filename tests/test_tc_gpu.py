@@ -79,3 +79,14 @@ def test_alignment_error():
     b = torch.ones(27, 64, device="cuda")
     with pytest.raises(nat.BadProblemShape):
         _gemm().matmul(a, b, (1, 1, 1, 8, 8), family="tf32")
+
+
+@pytest.mark.parametrize("family", ["bf16", "tf32"])
+@pytest.mark.parametrize("ta,tb", [(False, False), (False, True), (True, False), (True, True)])
+def test_runtime_selection_every_layout(family, ta, tb):
+    """kp_gemm_auto has a compiled selector for every tensor-core layout;
+    the selected kernel stays within the K-scaled bound."""
+    gemm = _gemm()
+    for (m, k, n) in [(200, 576, 64), (1000, 128, 264)]:
+        cfg = gemm.select(m, k, n, family=family, trans_a=ta, trans_b=tb)
+        _check(family, cfg, m, k, n, ta, tb, seed=m + k + n)
