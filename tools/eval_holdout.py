@@ -27,14 +27,15 @@ from paper_2003_06795_b200.pipeline import load_matrix  # noqa: E402
 
 def main() -> int:
     ap = argparse.ArgumentParser()
-    ap.add_argument("datasets", nargs="+", help="path:trans")
+    ap.add_argument("datasets", nargs="+", help="path:trans or path:family_trans")
     ap.add_argument("--out")
     args = ap.parse_args()
     doc = {"generator": "tools/eval_holdout.py", "variants": {}}
     for spec in args.datasets:
-        path, trans = spec.rsplit(":", 1)
+        path, variant = spec.rsplit(":", 1)
+        variant = variant if "_" in variant else f"f32_{variant}"
         matrix = load_matrix(path)
-        sel_dir = ROOT / "selectors" / f"f32_{trans}"
+        sel_dir = ROOT / "selectors" / variant
         model = selector_models.load_model(sel_dir / "model.json")
         selection = pruning.load_selection(sel_dir / "selection.json", matrix.configs)
         score = selector_models.evaluate_model(model, matrix)
@@ -46,13 +47,13 @@ def main() -> int:
             rows.append({"mkn": list(prob.as_tuple()), "selected": list(cfg.as_tuple()),
                          "pct_of_best": 100.0 * float(matrix.values[i][j])})
         worst = sorted(rows, key=lambda r: r["pct_of_best"])[:5]
-        doc["variants"][f"f32_{trans}"] = {
+        doc["variants"][variant] = {
             "dataset": path, "problems": len(matrix.problems),
             "selector_pct_oracle_best": score.percent, "pruned_set_ceiling_pct": ceiling.percent,
             "geomean_check": 100.0 * math.exp(sum(math.log(r["pct_of_best"] / 100.0)
                                                   for r in rows) / len(rows)),
             "worst": worst, "rows": rows}
-        print(f"f32_{trans}: {len(rows)} unseen problems, selector {score.percent:.2f} % of "
+        print(f"{variant}: {len(rows)} unseen problems, selector {score.percent:.2f} % of "
               f"oracle-best (pruned-set ceiling {ceiling.percent:.2f} %)")
     if args.out:
         Path(args.out).write_text(json.dumps(doc, indent=1) + "\n")
