@@ -58,19 +58,20 @@ def test_compiled_selector_matches_committed_model():
             assert got == codegen.traverse_document(doc, p.m, p.k, p.n), p
 
 
-@pytest.mark.parametrize("trans", ["nn", "nt"])
-def test_compiled_selector_generalises_to_unseen_batches(trans):
-    """The committed FP32 selector (trained on batch 1-16 network shapes +
+@pytest.mark.parametrize("variant", [f"{f}_{t}" for f in ("f32", "tf32", "bf16")
+                                     for t in ("nn", "nt", "tn", "tt")])
+def test_compiled_selector_generalises_to_unseen_batches(variant):
+    """Each committed selector (trained on batch 1-16 network shapes +
     squares) on the batch-32/64 network shapes it never saw, measured on the
-    B200 (data/b200_f32_<trans>_unseen.csv.gz, tools/eval_holdout.py):
+    B200 (data/b200_<variant>_unseen.csv.gz, tools/eval_holdout.py):
     north_star's >= 90 % geomean of the per-size oracle-best."""
     from paper_2003_06795_b200.pipeline import load_matrix
-    matrix = load_matrix(ROOT / "data" / f"b200_f32_{trans}_unseen.csv.gz")
-    model = selector_models.load_model(ROOT / "selectors" / f"f32_{trans}" / "model.json")
+    matrix = load_matrix(ROOT / "data" / f"b200_{variant}_unseen.csv.gz")
+    model = selector_models.load_model(ROOT / "selectors" / variant / "model.json")
     train = {p.as_tuple() for p in load_matrix(
-        ROOT / "data" / f"b200_f32_{trans}_train.csv.gz").problems}
+        ROOT / "data" / f"b200_{variant}_train.csv.gz").problems}
     assert not train & {p.as_tuple() for p in matrix.problems}
     score = selector_models.evaluate_model(model, matrix).percent
     profile = json.loads((ROOT / "profiles" / "selector_unseen_r01.json").read_text())
-    assert abs(score - profile["variants"][f"f32_{trans}"]["selector_pct_oracle_best"]) < 1e-9
+    assert abs(score - profile["variants"][variant]["selector_pct_oracle_best"]) < 1e-9
     assert score >= 90.0, score
