@@ -130,16 +130,20 @@ def run_reference(args) -> int:
 # -------------------------------------------------------------- GPU helpers
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 20 ms (plus one
-    sample right after the region if the region was shorter than a period)."""
+    """nvidia-smi clocks / throttle reasons sampled every 20 ms. The sampler
+    is started before the warm-up steps (nvidia-smi needs ~0.1 s to produce
+    its first line) and the timed region is marked with host timestamps;
+    samples inside the region are kept. A region shorter than the sampling
+    period keeps the samples bracketing it (noted in the record)."""
 
-    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    QUERY = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self):
         self.proc = None
         self.path = None
+        self.begin = self.end = None
 
     def start(self):
         fd, self.path = tempfile.mkstemp(suffix=".csv")
@@ -151,29 +155,55 @@ class ClockSampler:
         except OSError:
             self.proc = None
 
+    def mark_begin(self):
+        self.begin = time.time()
+
+    def mark_end(self):
+        self.end = time.time()
+
+    def _rows(self, gpu_index):
+        import datetime
+        rows = []
+        for line in Path(self.path).read_text().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 10 or f[1] != str(gpu_index):
+                continue
+            try:
+                ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                rows.append((ts, float(f[2]), float(f[3]), f[6:10]))
+            except ValueError:
+                continue
+        return rows
+
     def stop(self, gpu_index: int) -> dict:
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.05)
+        end = self.end or time.time()
+        deadline = time.time() + 2.0
+        while time.time() < deadline:  # until a sample after the region exists
+            rows = self._rows(gpu_index)
+            if rows and rows[-1][0] >= end:
+                break
+            time.sleep(0.02)
         self.proc.terminate()
         self.proc.wait()
-        mhz, mx, reasons = [], None, set()
-        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for line in Path(self.path).read_text().splitlines():
-            f = [x.strip() for x in line.split(",")]
-            if len(f) < 9 or f[0] != str(gpu_index):
-                continue
-            try:
-                mhz.append(float(f[1]))
-                mx = float(f[2])
-            except ValueError:
-                continue
-            for name, val in zip(names, f[5:9]):
-                if val.lower() == "active":
-                    reasons.add(name)
+        rows = self._rows(gpu_index)
         os.unlink(self.path)
-        return {"sm_mhz": statistics.median(mhz) if mhz else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(mhz)}
+        begin = self.begin or end
+        inside = [r for r in rows if begin <= r[0] <= end]
+        note = "samples inside the timed region"
+        if not inside and rows:
+            before = [r for r in rows if r[0] < begin][-1:]
+            after = [r for r in rows if r[0] > end][:1]
+            inside = before + after
+            note = "region shorter than the 20 ms period: the samples bracketing it"
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = {n for r in inside for n, v in zip(names, r[3]) if v.lower() == "active"}
+        mhz = [r[1] for r in inside]
+        return {"sm_mhz": statistics.median(mhz) if mhz else None,
+                "sm_max_mhz": inside[-1][2] if inside else None,
+                "reasons": sorted(reasons), "samples": len(inside), "sampling": note,
+                "region_s": round(end - begin, 4)}
 
 
 def gpu_index() -> int:
@@ -275,11 +305,13 @@ class FamilyRun:
         ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in SIZES] for _ in range(n)]
         launches0 = 0
+        if clocks:
+            clocks.start()
         for step in range(n):
             if step == self.args.warmup:
                 self.barrier()
                 if clocks:
-                    clocks.start()
+                    clocks.mark_begin()
                 launches0 = self.gemm.launch_count()
             for i, (s, a, b, c) in enumerate(self.probs):
                 flush.zero_()
@@ -287,6 +319,8 @@ class FamilyRun:
                 self.gemm.matmul(a, b, None, out=c, family=self.family)
                 ev[step][i][1].record(stream)
         self.barrier()
+        if clocks:
+            clocks.mark_end()
         launches = self.gemm.launch_count() - launches0
         ms = np.array([[ev[st][i][0].elapsed_time(ev[st][i][1]) for i in range(len(SIZES))]
                        for st in range(self.args.warmup, n)])
