@@ -1,0 +1,74 @@
+"""bench.py contract on CPU: the committed bench lines carry every key the
+driver and the judge read, and the host-side helpers (clock sampling, the
+e2e row blocking) behave as documented -- no GPU needed."""
+
+import json
+import sys
+import types
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+KEYS = ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+        "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config", "e2e",
+        "gpu_launches", "clocks", "roofline", "cpu_baseline")
+
+
+def test_committed_bench_line_has_contract_keys():
+    line = json.loads((ROOT / "profiles" / "bench_r01.json").read_text())
+    for k in KEYS:
+        assert k in line, k
+    assert line["warmup"] >= 3 and line["gpu_launches"] > 0
+    assert set(line["e2e"]) >= {"value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"}
+    assert line["e2e"]["h2d_bytes_per_step"] > 0 and line["e2e"]["d2h_bytes_per_step"] > 0
+    roof = line["roofline"]
+    assert set(roof) >= {"bound", "achieved", "peak", "unit", "frac", "traffic"}
+    assert abs(roof["frac"] - roof["achieved"] / roof["peak"]) < 1e-9
+    assert set(line["cpu_baseline"]) >= {"value", "unit", "cores", "kind", "sample"}
+    assert line["clocks"]["samples"] >= 1 and line["clocks"]["sm_mhz"]
+    assert "workload" in line["config"] and "l2" in line["config"]
+
+
+def test_reference_arm_line():
+    line = json.loads((ROOT / "profiles" / "bench_ref_r01.json").read_text())
+    assert line["impl"] == "reference"
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
+    assert line["cpu_baseline"]["value"] == line["value"]
+
+
+def test_clock_sampler_keeps_samples_inside_the_region(tmp_path):
+    import bench
+    cs = bench.ClockSampler()
+    cs.path = str(tmp_path / "clk.csv")
+    rows = []
+    for i, mhz in enumerate((1000, 1965, 1965, 1965, 1200)):
+        rows.append(f"2026/10/17 12:00:00.{100 * i + 50:03d}, 0, {mhz}, 1965, 900.0, 0x0, "
+                    f"Not Active, Not Active, Not Active, {'Active' if i == 2 else 'Not Active'}")
+    Path(cs.path).write_text("\n".join(rows) + "\n")
+    import datetime
+    t0 = datetime.datetime(2026, 10, 17, 12, 0, 0).timestamp()
+    cs.proc = types.SimpleNamespace(terminate=lambda: None, wait=lambda: None)
+    cs.begin, cs.end = t0 + 0.1, t0 + 0.36
+    rec = cs.stop(0)
+    assert rec["samples"] == 3 and rec["sm_mhz"] == 1965 and rec["reasons"] == ["sw_power_cap"]
+    # a region shorter than the sampling period keeps the bracketing samples
+    Path(cs.path).write_text("\n".join(rows) + "\n")
+    cs.begin, cs.end = t0 + 0.16, t0 + 0.17
+    rec = cs.stop(0)
+    assert rec["samples"] == 2 and "bracketing" in rec["sampling"]
+
+
+@pytest.mark.parametrize("m,k,want", [(2048, 2048, 4), (2100, 700, 2), (512, 512, 1), (300, 27, 1),
+                                      (100000, 64, 7)])
+def test_pinned_pipeline_row_blocks(m, k, want):
+    torch = pytest.importorskip("torch")
+    from paper_2003_06795_b200.gemm import PinnedPipeline
+    fake = types.SimpleNamespace(family="f32", CHUNK_BYTES=PinnedPipeline.CHUNK_BYTES,
+                                 MIN_ROWS=PinnedPipeline.MIN_ROWS)
+    blocks = PinnedPipeline._blocks(fake, torch.empty((m, k)))
+    assert blocks[0][0] == 0 and blocks[-1][1] == m
+    assert all(a[1] == b[0] for a, b in zip(blocks, blocks[1:]))
+    assert len(blocks) == want
