@@ -99,6 +99,40 @@ def cpu_baseline(seconds: float) -> dict:
                       f"({spent:.1f} s, OpenBLAS all threads)"}
 
 
+def host_pipeline(cells, configs) -> dict:
+    """the reference's own CPU sweep path
+    (synthetic.generate, the analytic stand-in for measuring a config) on the
+    same configs x sizes cells, and the selection pipeline (prune -> decision
+    tree -> C header) on this run's measured sweep -- the reference
+    algorithms, restated bit-exactly in this package, timed on one host core."""
+    import numpy as np
+    from paper_2003_06795_b200 import codegen, dataset, pruning, selector_models, synthetic
+    from paper_2003_06795_b200.dataset import ProblemSize
+    problems = tuple(ProblemSize(s, s, s) for s in SIZES)
+    spec = synthetic.SyntheticSpec(problems, seed=42)
+    t0 = time.perf_counter()
+    n = 0
+    while time.perf_counter() - t0 < 1.0 or n == 0:
+        synthetic.generate(spec)
+        n += 1
+    gen_s = (time.perf_counter() - t0) / n
+    grid = np.array([[2.0 * s ** 3 / cells[(i, j)] for j in range(len(configs))]
+                     for i, s in enumerate(SIZES)])
+    matrix = dataset.normalize(dataset.PerformanceMatrix(problems, tuple(configs), grid))
+    t0 = time.perf_counter()
+    sel = pruning.prune("top-count", matrix, 4, 42)
+    t1 = time.perf_counter()
+    model = selector_models.train_model("decision-tree", selector_models.make_labels(matrix, sel), 42)
+    t2 = time.perf_counter()
+    codegen.emit_selector_source(codegen.export_tree(model), "select_kernel")
+    t3 = time.perf_counter()
+    return {"synthetic_generate_cells_per_s": len(problems) * len(configs) / gen_s,
+            "prune_top_count_ms": 1e3 * (t1 - t0), "train_decision_tree_ms": 1e3 * (t2 - t1),
+            "codegen_ms": 1e3 * (t3 - t2), "cores": 1,
+            "what": "reference algorithms (bit-exact restatement) on this run's cells: the "
+                    "analytic sweep stand-in, and prune/train/codegen on the measured sweep"}
+
+
 def run_reference(args) -> int:
     """--impl reference: the CPU implementation of the path (numpy fp32 GEMM
     over the same workload) on the box's host cores; rank 0 only."""
@@ -478,6 +512,8 @@ def run_gpu(args) -> int:
     }
     if world == 1:
         line["cpu_baseline"] = cpu_baseline(args.cpu_seconds)
+        if f32.cells:
+            line["host_pipeline"] = host_pipeline(f32.cells, f32.configs)
     print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
