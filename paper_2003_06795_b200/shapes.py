@@ -91,10 +91,13 @@ PROBLEM_SETS = {
     "networks-all": lambda: network_problems(),
     "networks-small": lambda: network_problems(batches=(1, 4), max_flops=2e9),
     # selector training set: the network shapes plus the bench's square sizes
-    # (and 4096) so the deployed tree also covers BASELINE configs[1]
+    # (and 4096, 8192) so the deployed tree also covers BASELINE configs[1]
+    # and the large-size regime of north_star
     "networks+squares": lambda: tuple(dict.fromkeys(
         network_problems(batches=(1, 2, 4, 8, 16))
-        + square_problems((64, 128, 256, 512, 1024, 2048, 4096)))),
+        + square_problems((64, 128, 256, 512, 1024, 2048, 4096, 8192)))),
+    # the row added to the round-1 datasets after their first sweep
+    "square-8192": lambda: square_problems((8192,)),
     # generalisation check: the batch-32/64 network shapes the selectors were
     # never trained on (BASELINE configs[2] spans batch 1-64)
     "networks-unseen": lambda: tuple(
