@@ -156,6 +156,50 @@ def plan_shards(problems, n_shards: int, batch: int = 1) -> list[list[int]]:
     return [sorted(s) for s in shards]
 
 
+def plan_tasks(problems, n_devices: int, n_configs: int, batch: int = 1,
+               granularity: int = 4) -> list[tuple[int, int, int]]:
+    """Sweep tasks (problem, first config, end config), longest first, for a
+    dynamic queue over `n_devices` workers. A problem costing more than
+    total / (granularity * n_devices) is cut into contiguous config ranges
+    (at most 16), so one huge problem (8192^3) cannot hold the last worker
+    while the others idle; everything else stays one task per problem
+    (operands generated once)."""
+    if n_devices < 1:
+        raise ValueError("n_devices must be >= 1")
+    costs = [problem_cost(p, batch) for p in problems]
+    limit = sum(costs) / (granularity * n_devices)
+    tasks = []
+    for i, c in enumerate(costs):
+        k = 1 if n_devices == 1 else min(16, n_configs, max(1, -(-int(c) // max(1, int(limit)))))
+        bounds = [round(j * n_configs / k) for j in range(k + 1)]
+        tasks += [(i, bounds[j], bounds[j + 1], c * (bounds[j + 1] - bounds[j]) / n_configs)
+                  for j in range(k)]
+    tasks.sort(key=lambda t: (-t[3], t[0], t[1]))
+    return [(i, lo, hi) for i, lo, hi, _ in tasks]
+
+
+def merge_chunks(n_problems: int, n_configs: int, chunks) -> np.ndarray:
+    """Reassemble (problem, lo, hi, runtimes[hi-lo]) chunks into the (P, C)
+    grid; every cell must arrive exactly once (complete-grid contract)."""
+    grid = np.full((n_problems, n_configs), np.nan)
+    count = np.zeros((n_problems, n_configs), dtype=np.int64)
+    for i, lo, hi, row in chunks:
+        row = np.asarray(row, dtype=float)
+        if row.shape != (hi - lo,):
+            raise RuntimeError(f"chunk ({i}, {lo}, {hi}) has {row.shape[0]} runtimes")
+        grid[i, lo:hi] = row
+        count[i, lo:hi] += 1
+    if (count > 1).any():
+        i, j = np.argwhere(count > 1)[0]
+        raise RuntimeError(f"cell ({i}, {j}) measured twice")
+    if (count == 0).any():
+        missing = sorted({int(i) for i, _ in np.argwhere(count == 0)})
+        raise RuntimeError(f"problems never fully measured: {missing}")
+    if not np.isfinite(grid).all() or (grid <= 0).any():
+        raise RuntimeError("non-positive or non-finite runtime in sweep")
+    return grid
+
+
 def merge_shards(n_problems: int, n_configs: int, parts) -> np.ndarray:
     """Reassemble {problem index: runtimes row} parts into the (P, C) grid;
     every problem must arrive exactly once (complete-grid contract,
@@ -212,15 +256,17 @@ def _worker(device: int, spec: SweepSpec, task_q, result_q) -> None:
         configs = (tuple(spec.configs) if spec.configs is not None
                    else gemm.family_configs(spec.family))
         while True:
-            i = task_q.get()
-            if i is None:
+            task = task_q.get()
+            if task is None:
                 break
+            i, lo, hi = task
             a, b = _operands(spec.problems[i], spec, i, torch.device("cuda", 0))
-            row = gemm.sweep_problem(a, b, configs, family=spec.family, warmup=spec.warmup,
-                                     reps=spec.reps, min_sample_ns=spec.min_sample_ns,
+            row = gemm.sweep_problem(a, b, configs[lo:hi], family=spec.family,
+                                     warmup=spec.warmup, reps=spec.reps,
+                                     min_sample_ns=spec.min_sample_ns,
                                      max_cell_ns=spec.max_cell_ns)
             del a, b
-            result_q.put(("row", device, i, row))
+            result_q.put(("row", device, (i, lo, hi), row))
         result_q.put(("done", device, device_facts(0), None))
     except Exception as exc:  # surfaced by the parent; never silently imputed
         result_q.put(("error", device, repr(exc), None))
@@ -228,27 +274,28 @@ def _worker(device: int, spec: SweepSpec, task_q, result_q) -> None:
 
 def run_sharded(spec: SweepSpec, devices) -> SweepResult:
     """Sweep across several GPUs: a dynamic longest-first work queue of
-    problems, one worker process per GPU, no device-to-device traffic.
-    A worker error aborts the sweep (a failed cell is never imputed)."""
+    (problem, config range) tasks (plan_tasks), one worker process per GPU,
+    no device-to-device traffic. A worker error aborts the sweep (a failed
+    cell is never imputed)."""
     import multiprocessing as mp
+    from . import gemm
+    n_cfg = len(spec.configs) if spec.configs is not None else len(gemm.family_configs(spec.family))
     ctx = mp.get_context("spawn")
     task_q, result_q = ctx.Queue(), ctx.Queue()
-    order = sorted(range(len(spec.problems)),
-                   key=lambda i: (-problem_cost(spec.problems[i], spec.batch), i))
-    for i in order:
-        task_q.put(i)
+    for task in plan_tasks(spec.problems, len(devices), n_cfg, spec.batch):
+        task_q.put(task)
     for _ in devices:
         task_q.put(None)
     t0 = time.perf_counter()
     procs = [ctx.Process(target=_worker, args=(d, spec, task_q, result_q)) for d in devices]
     for p in procs:
         p.start()
-    rows, done, facts = {}, 0, {}
+    chunks, done, facts = [], 0, {}
     try:
         while done < len(devices):
             kind, dev, a, b = result_q.get()
             if kind == "row":
-                rows[a] = b
+                chunks.append((a[0], a[1], a[2], b))
             elif kind == "done":
                 done += 1
                 facts[dev] = a
@@ -260,11 +307,7 @@ def run_sharded(spec: SweepSpec, devices) -> SweepResult:
             if p.is_alive():
                 p.terminate()
     wall = time.perf_counter() - t0
-    from . import gemm
-    n_cfg = len(spec.configs) if spec.configs is not None else None
-    if n_cfg is None:
-        n_cfg = len(next(iter(rows.values())))
-    grid = merge_shards(len(spec.problems), n_cfg, [rows])
+    grid = merge_chunks(len(spec.problems), n_cfg, chunks)
     configs = tuple(spec.configs) if spec.configs is not None else gemm.family_configs(spec.family)
     first = facts[min(facts)] if facts else {}
     return SweepResult(spec, configs, grid, wall, dict(first, devices=len(devices)))

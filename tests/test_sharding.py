@@ -103,3 +103,40 @@ def test_bench_reductions_world2():
     out = manager.dict()
     mp.spawn(_reduce_worker, args=(2, port, out), nprocs=2, join=True)
     assert out[0] == out[1] == (2.5, 30.0)
+
+
+def test_plan_tasks_splits_only_dominant_problems_and_covers_every_cell():
+    import numpy as np
+    from paper_2003_06795_b200 import measure, shapes
+    probs = shapes.problem_set("networks+squares")
+    assert measure.plan_tasks(probs, 1, 640) == [(i, 0, 640) for i in
+                                                 [t[0] for t in measure.plan_tasks(probs, 1, 640)]]
+    for nd in (2, 4, 8):
+        tasks = measure.plan_tasks(probs, nd, 640)
+        cover = np.zeros((len(probs), 640), dtype=int)
+        for i, lo, hi in tasks:
+            assert 0 <= lo < hi <= 640
+            cover[i, lo:hi] += 1
+        assert (cover == 1).all()
+        split = {probs[i].as_tuple() for i, lo, hi in tasks if (lo, hi) != (0, 640)}
+        assert (8192, 8192, 8192) in split
+        costs = [measure.problem_cost(p) for p in probs]
+        # longest first: task costs are non-increasing along the queue
+        per_task = [costs[i] * (hi - lo) / 640 for i, lo, hi in tasks]
+        assert per_task == sorted(per_task, reverse=True)
+
+
+def test_merge_chunks_contract():
+    import numpy as np
+    import pytest
+    from paper_2003_06795_b200 import measure
+    chunks = [(0, 0, 3, [1.0, 2.0, 3.0]), (1, 0, 2, [4.0, 5.0]), (1, 2, 3, [6.0])]
+    grid = measure.merge_chunks(2, 3, chunks)
+    assert grid.tolist() == [[1, 2, 3], [4, 5, 6]]
+    with pytest.raises(RuntimeError, match="twice"):
+        measure.merge_chunks(2, 3, chunks + [(1, 2, 3, [7.0])])
+    with pytest.raises(RuntimeError, match="never fully measured"):
+        measure.merge_chunks(2, 3, chunks[:2])
+    with pytest.raises(RuntimeError, match="non-positive"):
+        measure.merge_chunks(1, 1, [(0, 0, 1, [0.0])])
+    assert np.isfinite(grid).all()
