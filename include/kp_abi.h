@@ -119,6 +119,18 @@ kp_status kp_sweep_problem(kp_family family, const kp_config* cfgs, int32_t n_cf
                            double min_sample_ns, double max_cell_ns,
                            double* runtime_ns, void* stream);
 
+/* kp_sweep_problem with explicit policy flags.  KP_SWEEP_EARLY_EXIT enables
+ * the hopeless-config early exit described above (kp_sweep_problem always
+ * sets it); without it every config gets the full warm-up + reps statistic --
+ * what a sweep split into config ranges needs, since only a call that sees a
+ * whole problem knows its best median. */
+#define KP_SWEEP_EARLY_EXIT 1
+kp_status kp_sweep_problem_ex(kp_family family, const kp_config* cfgs, int32_t n_cfgs,
+                              const kp_gemm_desc* desc, const void* A, const void* B,
+                              float* C, int32_t warmup, int32_t reps,
+                              double min_sample_ns, double max_cell_ns, int32_t flags,
+                              double* runtime_ns, void* stream);
+
 /* K1 (FP32 SIMT) tile scheduling.  0 = one output tile per CTA; 1 (default)
  * = ordered stream-K when whole tiles would leave part of the last wave idle:
  * one persistent wave shares the (tile, k-slice) units evenly, a tile split

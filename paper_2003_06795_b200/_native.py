@@ -32,7 +32,7 @@ EXPORTS = ("kp_abi_version", "kp_num_configs", "kp_config_at", "kp_config_valid"
            "kp_gemm", "kp_gemm_time", "kp_sweep_problem", "kp_select", "kp_gemm_auto",
            "kp_status_string", "kp_last_error", "kp_launch_count", "kp_device_info",
            "kp_fp32_peak", "kp_conv_output_shape", "kp_im2col", "kp_conv2d_auto",
-           "kp_set_schedule")
+           "kp_set_schedule", "kp_sweep_problem_ex")
 
 
 class KpConfig(ctypes.Structure):
@@ -94,6 +94,10 @@ def _declare(lib):
                                        c.c_void_p, c.c_void_p, c.c_void_p, c.c_int32,
                                        c.c_int32, c.c_double, c.c_double, P(c.c_double),
                                        c.c_void_p]),
+        "kp_sweep_problem_ex": (c.c_int, [c.c_int, P(KpConfig), c.c_int32, P(KpGemmDesc),
+                                          c.c_void_p, c.c_void_p, c.c_void_p, c.c_int32,
+                                          c.c_int32, c.c_double, c.c_double, c.c_int32,
+                                          P(c.c_double), c.c_void_p]),
         "kp_select": (c.c_int, [c.c_int, c.c_int32, c.c_int32, c.c_int64, c.c_int64,
                                 c.c_int64, P(KpConfig)]),
         "kp_gemm_auto": (c.c_int, [c.c_int, P(KpGemmDesc), c.c_void_p, c.c_void_p,

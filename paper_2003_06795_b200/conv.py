@@ -13,7 +13,7 @@ from __future__ import annotations
 import ctypes
 
 from . import _native as nat
-from .gemm import _family_dtype, _stream_handle, _torch
+from .gemm import _family_dtype, _stream_handle, _torch, check_device
 
 
 def _desc(x, w, stride, padding) -> nat.KpConvDesc:
@@ -43,6 +43,7 @@ def im2col(x, kh: int, kw: int, stride=1, padding=0, family="f32"):
     fam = nat.family_id(family)
     if x.dtype != _family_dtype(fam):
         raise nat.BadProblemShape(f"family {family!r} expects {_family_dtype(fam)} input")
+    check_device(x)
     w_shape = (1, x.shape[1], kh, kw)
     ho, wo = output_shape(x.shape, w_shape, stride, padding)
     x = x.contiguous()
@@ -51,8 +52,9 @@ def im2col(x, kh: int, kw: int, stride=1, padding=0, family="f32"):
     d = nat.KpConvDesc(x.shape[0], x.shape[1], x.shape[2], x.shape[3], 1, kh, kw,
                        *((stride, stride) if isinstance(stride, int) else stride),
                        *((padding, padding) if isinstance(padding, int) else padding))
-    nat.check(nat.lib().kp_im2col(fam, ctypes.byref(d), x.data_ptr(), cols.data_ptr(),
-                                  _stream_handle()), "kp_im2col")
+    with torch.cuda.device(x.device):
+        nat.check(nat.lib().kp_im2col(fam, ctypes.byref(d), x.data_ptr(), cols.data_ptr(),
+                                      _stream_handle(x.device)), "kp_im2col")
     return cols
 
 
@@ -65,6 +67,7 @@ def conv2d(x, w, stride=1, padding=0, *, family="f32", nhwc: bool = False, works
     want = _family_dtype(fam)
     if x.dtype != want or w.dtype != want:
         raise nat.BadProblemShape(f"family {family!r} expects {want} tensors")
+    check_device(x, w, workspace)
     d = _desc(x, w, stride, padding)
     ho, wo = output_shape(x.shape, w.shape, stride, padding)
     m, k = d.batch * ho * wo, d.c_in * d.kh * d.kw
@@ -74,7 +77,9 @@ def conv2d(x, w, stride=1, padding=0, *, family="f32", nhwc: bool = False, works
         workspace = torch.empty(m * k, dtype=want, device=x.device)
     y = torch.empty((d.batch, ho, wo, d.c_out), dtype=torch.float32, device=x.device)
     chosen = nat.KpConfig()
-    nat.check(nat.lib().kp_conv2d_auto(fam, ctypes.byref(d), x.data_ptr(), wmat.data_ptr(),
-                                       y.data_ptr(), workspace.data_ptr(), _stream_handle(),
-                                       ctypes.byref(chosen)), "kp_conv2d_auto")
+    with torch.cuda.device(x.device):
+        nat.check(nat.lib().kp_conv2d_auto(fam, ctypes.byref(d), x.data_ptr(), wmat.data_ptr(),
+                                           y.data_ptr(), workspace.data_ptr(),
+                                           _stream_handle(x.device), ctypes.byref(chosen)),
+                  "kp_conv2d_auto")
     return y if nhwc else y.permute(0, 3, 1, 2)

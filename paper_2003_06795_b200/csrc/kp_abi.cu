@@ -300,22 +300,26 @@ kp_status kp_gemm_time(kp_family family, kp_config cfg, const kp_gemm_desc* desc
                     static_cast<cudaStream_t>(stream));
 }
 
-kp_status kp_sweep_problem(kp_family family, const kp_config* cfgs, int32_t n_cfgs,
-                           const kp_gemm_desc* desc, const void* A, const void* B, float* C,
-                           int32_t warmup, int32_t reps, double min_sample_ns, double max_cell_ns,
-                           double* runtime_ns, void* stream) {
+kp_status kp_sweep_problem_ex(kp_family family, const kp_config* cfgs, int32_t n_cfgs,
+                              const kp_gemm_desc* desc, const void* A, const void* B, float* C,
+                              int32_t warmup, int32_t reps, double min_sample_ns,
+                              double max_cell_ns, int32_t flags, double* runtime_ns, void* stream) {
     if (!cfgs || !runtime_ns || n_cfgs < 0) return fail(KP_ERR_INVALID_ARG, "bad sweep arguments");
+    if (flags & ~int32_t(KP_SWEEP_EARLY_EXIT)) return fail(KP_ERR_INVALID_ARG, "unknown sweep flags");
     kp_status st;
     GemmProblem g;
     if ((st = to_problem(desc, A, B, C, &g)) != KP_OK) return st;
     for (int32_t i = 0; i < n_cfgs; ++i)
         if ((st = valid_config(family, cfgs[i])) != KP_OK) return st;
-    // A config whose first launch is both over 1 ms and 8x the best median of
-    // this problem so far keeps that single timing: it normalises below
-    // 0.125 either way and the extra launches would dominate the sweep.
+    // With KP_SWEEP_EARLY_EXIT, a config whose first launch is both over 1 ms
+    // and 8x the best median of this call so far keeps that single timing: it
+    // normalises below 0.125 either way and the extra launches would dominate
+    // the sweep. Callers timing only part of a problem's configs clear the
+    // flag, so every cell gets the same statistic as in a whole-problem call.
+    const bool early = (flags & KP_SWEEP_EARLY_EXIT) != 0;
     double best = 0.0;
     for (int32_t i = 0; i < n_cfgs; ++i) {
-        const double hopeless = best > 0.0 ? std::max(1e6, 8.0 * best) : 0.0;
+        const double hopeless = early && best > 0.0 ? std::max(1e6, 8.0 * best) : 0.0;
         st = time_one(family, cfgs[i], g, warmup, reps, min_sample_ns, max_cell_ns,
                       runtime_ns + i, static_cast<cudaStream_t>(stream), hopeless);
         if (st == KP_OK && (best == 0.0 || runtime_ns[i] < best)) best = runtime_ns[i];
@@ -328,6 +332,14 @@ kp_status kp_sweep_problem(kp_family family, const kp_config* cfgs, int32_t n_cf
         }
     }
     return KP_OK;
+}
+
+kp_status kp_sweep_problem(kp_family family, const kp_config* cfgs, int32_t n_cfgs,
+                           const kp_gemm_desc* desc, const void* A, const void* B, float* C,
+                           int32_t warmup, int32_t reps, double min_sample_ns, double max_cell_ns,
+                           double* runtime_ns, void* stream) {
+    return kp_sweep_problem_ex(family, cfgs, n_cfgs, desc, A, B, C, warmup, reps, min_sample_ns,
+                               max_cell_ns, KP_SWEEP_EARLY_EXIT, runtime_ns, stream);
 }
 
 kp_status kp_select(kp_family family, int32_t trans_a, int32_t trans_b, int64_t m, int64_t k,

@@ -66,8 +66,7 @@ def describe(a, b, out=None, alpha: float = 1.0, beta: float = 0.0, family="f32"
     if a.dtype != want or b.dtype != want:
         raise nat.BadProblemShape(f"family {family!r} expects {want} operands, "
                                   f"got {a.dtype} and {b.dtype}")
-    if not (a.is_cuda and b.is_cuda):
-        raise nat.KernelLibraryError("operands must be CUDA tensors (no CPU fallback)")
+    check_device(a, b, out)
     m, k = a.shape[-2], a.shape[-1]
     k2, n = b.shape[-2], b.shape[-1]
     if k != k2:
@@ -96,9 +95,27 @@ def describe(a, b, out=None, alpha: float = 1.0, beta: float = 0.0, family="f32"
     return desc, a, b, out
 
 
-def _stream_handle():
+def check_device(*tensors):
+    """All tensors (None skipped) are CUDA tensors on one device; returns it.
+    A CPU tensor or a second device would otherwise reach the kernels as a
+    foreign pointer and fault the context instead of raising."""
+    devs = {t.device for t in tensors if t is not None}
+    if any(d.type != "cuda" for d in devs):
+        raise nat.KernelLibraryError("operands must be CUDA tensors (no CPU fallback)")
+    if len(devs) != 1:
+        raise nat.BadProblemShape(f"operands live on different devices: {sorted(map(str, devs))}")
+    return devs.pop()
+
+
+def _stream_handle(device=None):
+    """The current stream of `device` (default: the current device)."""
     torch = _torch()
-    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def on_device(t):
+    """Context making t's device current, so the library launches there."""
+    return _torch().cuda.device(t.device)
 
 
 def matmul(a, b, config=None, *, family="f32", out=None, alpha: float = 1.0,
@@ -111,14 +128,16 @@ def matmul(a, b, config=None, *, family="f32", out=None, alpha: float = 1.0,
     fam = nat.family_id(family)
     desc, a, b, out = describe(a, b, out, alpha, beta, family)
     lib = nat.lib()
-    if config is None:
-        chosen = nat.KpConfig()
-        nat.check(lib.kp_gemm_auto(fam, ctypes.byref(desc), a.data_ptr(), b.data_ptr(),
-                                   out.data_ptr(), _stream_handle(), ctypes.byref(chosen)),
-                  "kp_gemm_auto")
-    else:
-        nat.check(lib.kp_gemm(fam, nat.to_kp_config(config), ctypes.byref(desc), a.data_ptr(),
-                              b.data_ptr(), out.data_ptr(), _stream_handle()), "kp_gemm")
+    with on_device(a):
+        if config is None:
+            chosen = nat.KpConfig()
+            nat.check(lib.kp_gemm_auto(fam, ctypes.byref(desc), a.data_ptr(), b.data_ptr(),
+                                       out.data_ptr(), _stream_handle(a.device),
+                                       ctypes.byref(chosen)), "kp_gemm_auto")
+        else:
+            nat.check(lib.kp_gemm(fam, nat.to_kp_config(config), ctypes.byref(desc),
+                                  a.data_ptr(), b.data_ptr(), out.data_ptr(),
+                                  _stream_handle(a.device)), "kp_gemm")
     return out
 
 
@@ -284,26 +303,32 @@ def time_config(a, b, config, *, family="f32", out=None, warmup: int = 3, reps: 
     fam = nat.family_id(family)
     desc, a, b, out = describe(a, b, out, 1.0, 0.0, family)
     res = ctypes.c_double()
-    nat.check(nat.lib().kp_gemm_time(fam, nat.to_kp_config(config), ctypes.byref(desc),
-                                     a.data_ptr(), b.data_ptr(), out.data_ptr(), warmup, reps,
-                                     min_sample_ns, max_cell_ns, ctypes.byref(res),
-                                     _stream_handle()),
-              "kp_gemm_time")
+    with on_device(a):
+        nat.check(nat.lib().kp_gemm_time(fam, nat.to_kp_config(config), ctypes.byref(desc),
+                                         a.data_ptr(), b.data_ptr(), out.data_ptr(), warmup,
+                                         reps, min_sample_ns, max_cell_ns, ctypes.byref(res),
+                                         _stream_handle(a.device)),
+                  "kp_gemm_time")
     return res.value
 
 
 def sweep_problem(a, b, configs, *, family="f32", out=None, warmup: int = 2, reps: int = 5,
-                  min_sample_ns: float = 50_000.0, max_cell_ns: float = 0.0) -> list[float]:
-    """Median runtime (ns) of every config on one problem (C++ timing loop)."""
+                  min_sample_ns: float = 50_000.0, max_cell_ns: float = 0.0,
+                  early_exit: bool = True) -> list[float]:
+    """Median runtime (ns) of every config on one problem (C++ timing loop,
+    kp_sweep_problem_ex). ``early_exit=False`` gives every config the full
+    statistic (config-range tasks of a split problem)."""
     fam = nat.family_id(family)
     desc, a, b, out = describe(a, b, out, 1.0, 0.0, family)
     cfgs = (nat.KpConfig * len(configs))(*[nat.to_kp_config(c) for c in configs])
     res = (ctypes.c_double * len(configs))()
-    nat.check(nat.lib().kp_sweep_problem(fam, cfgs, len(configs), ctypes.byref(desc),
-                                         a.data_ptr(), b.data_ptr(), out.data_ptr(), warmup,
-                                         reps, min_sample_ns, max_cell_ns, res,
-                                         _stream_handle()),
-              "kp_sweep_problem")
+    with on_device(a):
+        nat.check(nat.lib().kp_sweep_problem_ex(fam, cfgs, len(configs), ctypes.byref(desc),
+                                                a.data_ptr(), b.data_ptr(), out.data_ptr(),
+                                                warmup, reps, min_sample_ns, max_cell_ns,
+                                                1 if early_exit else 0, res,
+                                                _stream_handle(a.device)),
+                  "kp_sweep_problem_ex")
     return list(res)
 
 

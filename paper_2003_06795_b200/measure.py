@@ -49,6 +49,7 @@ class SweepResult:
     runtime_ns: np.ndarray           # (P, C)
     wall_s: float
     device: dict = field(default_factory=dict)
+    task_log: list = field(default_factory=list)   # per task: device, NVML clocks
 
     @property
     def cells(self) -> int:
@@ -118,18 +119,23 @@ def run_sweep(spec: SweepSpec, device: int = 0, progress=None) -> SweepResult:
     torch.cuda.set_device(device)
     configs = tuple(spec.configs) if spec.configs is not None else gemm.family_configs(spec.family)
     rt = np.zeros((len(spec.problems), len(configs)), dtype=np.float64)
+    log = []
+    nvml_index = _visible_index(device)
     t0 = time.perf_counter()
     for i, p in enumerate(spec.problems):
+        before = gpu_clocks(nvml_index)
         a, b = _operands(p, spec, i, torch.device("cuda", device))
         rt[i] = gemm.sweep_problem(a, b, configs, family=spec.family, warmup=spec.warmup,
                                    reps=spec.reps, min_sample_ns=spec.min_sample_ns,
                                    max_cell_ns=spec.max_cell_ns)
         del a, b
+        log.append({"task": [i, 0, len(configs)], "device": device,
+                    "clocks": {"before": before, "after": gpu_clocks(nvml_index)}})
         if progress:
             progress(i, p, rt[i])
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
-    return SweepResult(spec, configs, rt, wall, device_facts(device))
+    return SweepResult(spec, configs, rt, wall, device_facts(device), task_log=log)
 
 
 def problem_cost(p: ProblemSize, batch: int = 1) -> float:
@@ -245,9 +251,39 @@ def gather_cells(local: dict, world: int, group=None) -> dict:
     return merged
 
 
-def _worker(device: int, spec: SweepSpec, task_q, result_q) -> None:
-    """One process per GPU: pull problem indices until the queue is empty."""
-    os.environ["CUDA_VISIBLE_DEVICES"] = str(device)
+def gpu_clocks(index: int) -> dict | None:
+    """SM clock (MHz) and active throttle reasons of one GPU via NVML (None
+    when NVML is unavailable). Logged beside every sweep task."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        mhz = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+        mask = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+    except Exception:  # noqa: BLE001 - NVML missing or not permitted
+        return None
+    names = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+             0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
+    return {"sm_mhz": int(mhz), "reasons": sorted(n for bit, n in names.items() if mask & bit)}
+
+
+def _visible_index(device: int) -> int:
+    """NVML index of logical device `device` under the parent's CUDA_VISIBLE_DEVICES."""
+    vis = [v.strip() for v in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if v.strip()]
+    if device < len(vis) and vis[device].isdigit():
+        return int(vis[device])
+    return device
+
+
+def _worker(device: int, spec: SweepSpec, conn) -> None:
+    """One process per GPU: announce readiness, then run the (problem, config
+    range) tasks the parent hands over until it sends None. Each result
+    carries the NVML clocks sampled before and after the task. `conn` is this
+    worker's own duplex pipe (synchronous sends, nothing shared with other
+    workers, so a worker killed mid-message cannot wedge the others)."""
+    nvml_index = _visible_index(device)
+    os.environ["CUDA_VISIBLE_DEVICES"] = str(nvml_index)
+    task = None
     try:
         import torch
 
@@ -255,62 +291,215 @@ def _worker(device: int, spec: SweepSpec, task_q, result_q) -> None:
         torch.cuda.set_device(0)
         configs = (tuple(spec.configs) if spec.configs is not None
                    else gemm.family_configs(spec.family))
+        conn.send(("ready", device, None, device_facts(0)))
         while True:
-            task = task_q.get()
+            task = conn.recv()
             if task is None:
                 break
             i, lo, hi = task
+            before = gpu_clocks(nvml_index)
             a, b = _operands(spec.problems[i], spec, i, torch.device("cuda", 0))
+            # a config-range task must time exactly like the whole problem
+            # would: the early exit for hopeless configs compares against the
+            # best median so far, which only a whole-problem task knows
             row = gemm.sweep_problem(a, b, configs[lo:hi], family=spec.family,
                                      warmup=spec.warmup, reps=spec.reps,
                                      min_sample_ns=spec.min_sample_ns,
-                                     max_cell_ns=spec.max_cell_ns)
+                                     max_cell_ns=spec.max_cell_ns,
+                                     early_exit=(lo, hi) == (0, len(configs)))
             del a, b
-            result_q.put(("row", device, (i, lo, hi), row))
-        result_q.put(("done", device, device_facts(0), None))
+            conn.send(("row", device, task, (row, {"before": before,
+                                                   "after": gpu_clocks(nvml_index)})))
     except Exception as exc:  # surfaced by the parent; never silently imputed
-        result_q.put(("error", device, repr(exc), None))
+        conn.send(("error", device, task, repr(exc)))
+        raise SystemExit(1)
 
 
-def run_sharded(spec: SweepSpec, devices) -> SweepResult:
-    """Sweep across several GPUs: a dynamic longest-first work queue of
-    (problem, config range) tasks (plan_tasks), one worker process per GPU,
-    no device-to-device traffic. A worker error aborts the sweep (a failed
-    cell is never imputed)."""
+def _spec_key(spec: SweepSpec, n_cfg: int) -> dict:
+    return {"family": spec.family, "trans_a": spec.trans_a, "trans_b": spec.trans_b,
+            "batch": spec.batch, "problems": [p.as_tuple() for p in spec.problems],
+            "configs": n_cfg, "warmup": spec.warmup, "reps": spec.reps,
+            "min_sample_ns": spec.min_sample_ns, "max_cell_ns": spec.max_cell_ns,
+            "seed": spec.seed}
+
+
+class TaskCheckpoint:
+    """Per-task result shards of a sharded sweep (resume after a crash): one
+    JSON file per finished (problem, config range) task under `directory`,
+    plus spec.json naming the sweep they belong to (a mismatch is an error,
+    never a silent mix of two sweeps)."""
+
+    def __init__(self, directory, key: dict):
+        from pathlib import Path
+        self.dir = Path(directory)
+        self.dir.mkdir(parents=True, exist_ok=True)
+        meta = self.dir / "spec.json"
+        key = json.loads(json.dumps(key))  # tuples -> lists, as stored
+        if meta.exists():
+            if json.loads(meta.read_text()) != key:
+                raise RuntimeError(f"{meta} belongs to a different sweep; use a fresh directory")
+        else:
+            meta.write_text(json.dumps(key))
+
+    def _path(self, task):
+        i, lo, hi = task
+        return self.dir / f"task_p{i}_c{lo}-{hi}.json"
+
+    def load(self, task):
+        path = self._path(task)
+        if not path.exists():
+            return None
+        doc = json.loads(path.read_text())
+        return np.asarray(doc["runtime_ns"], dtype=float), doc.get("log", {})
+
+    def save(self, task, row, log):
+        path = self._path(task)
+        tmp = path.with_suffix(".tmp")
+        tmp.write_text(json.dumps({"runtime_ns": [float(x) for x in row], "log": log}))
+        os.replace(tmp, path)
+
+
+def run_sharded(spec: SweepSpec, devices, *, checkpoint_dir=None, max_task_attempts: int = 2,
+                max_restarts: int = 2, poll_s: float = 2.0, start_timeout_s: float = 600.0,
+                _worker_fn=None) -> SweepResult:
+    """Sweep across several GPUs: longest-first (problem, config range) tasks
+    (plan_tasks) handed one at a time to one worker process per GPU, no
+    device-to-device traffic.
+
+    Robustness (an 8-GPU sweep runs for hours):
+      * the parent polls its result queue and checks every worker's liveness,
+        so a worker that dies without a message (segfault, OOM kill, driver
+        abort) is detected instead of blocking the parent forever;
+      * the dead (or failed) worker's in-flight task is re-queued at the front
+        and the worker is restarted on its device (up to `max_restarts` per
+        device); a task that fails `max_task_attempts` times aborts the sweep
+        (a cell is never imputed);
+      * with `checkpoint_dir`, every finished task is written as a shard and
+        a re-run of the same sweep skips the tasks already on disk.
+    Every task's NVML clocks / throttle reasons go into the result's log."""
     import multiprocessing as mp
+    from collections import deque
+    from multiprocessing import connection as mp_connection
+
     from . import gemm
     n_cfg = len(spec.configs) if spec.configs is not None else len(gemm.family_configs(spec.family))
+    target = _worker_fn or _worker
     ctx = mp.get_context("spawn")
-    task_q, result_q = ctx.Queue(), ctx.Queue()
+    ckpt = TaskCheckpoint(checkpoint_dir, _spec_key(spec, n_cfg)) if checkpoint_dir else None
+    chunks, task_log = [], []
+    pending = deque()
     for task in plan_tasks(spec.problems, len(devices), n_cfg, spec.batch):
-        task_q.put(task)
-    for _ in devices:
-        task_q.put(None)
+        got = ckpt.load(task) if ckpt else None
+        if got is not None:
+            chunks.append((task[0], task[1], task[2], got[0]))
+            task_log.append(dict(got[1], task=list(task), resumed=True))
+        else:
+            pending.append(task)
+    slots = {}  # slot -> {"dev", "proc", "conn", "task", "ready", "started", "restarts"}
+
+    def spawn(slot, dev, restarts):
+        parent_conn, child_conn = ctx.Pipe(duplex=True)
+        proc = ctx.Process(target=target, args=(dev, spec, child_conn), daemon=True)
+        proc.start()
+        child_conn.close()
+        slots[slot] = {"dev": dev, "proc": proc, "conn": parent_conn, "task": None,
+                       "ready": False, "started": time.monotonic(), "restarts": restarts}
+
+    attempts: dict = {}
+    facts: dict = {}
+
+    def fail_task(slot, why):
+        s = slots.pop(slot)
+        task = s["task"]
+        s["conn"].close()
+        s["proc"].join(timeout=30)
+        if s["proc"].is_alive():
+            s["proc"].terminate()
+            s["proc"].join(timeout=10)
+        task_log.append({"event": "worker_lost", "device": s["dev"], "task": list(task or ()),
+                         "why": why})
+        if task is not None:
+            attempts[task] = attempts.get(task, 0) + 1
+            if attempts[task] >= max_task_attempts:
+                raise RuntimeError(f"sweep task {task} failed {attempts[task]} times "
+                                   f"(last on device {s['dev']}: {why})")
+            pending.appendleft(task)
+        if s["restarts"] < max_restarts and pending:
+            spawn(slot, s["dev"], s["restarts"] + 1)
+        if not slots and pending:
+            raise RuntimeError(f"every sweep worker was lost; {len(pending)} tasks left ({why})")
+
+    def hand_out(slot):
+        s = slots[slot]
+        s["task"] = pending.popleft() if pending else None
+        s["conn"].send(s["task"])
+        if s["task"] is None:
+            s["ready"] = "stopping"
+
+    def busy():
+        return pending or any(s["task"] is not None or s["ready"] is False
+                              for s in slots.values())
+
     t0 = time.perf_counter()
-    procs = [ctx.Process(target=_worker, args=(d, spec, task_q, result_q)) for d in devices]
-    for p in procs:
-        p.start()
-    chunks, done, facts = [], 0, {}
     try:
-        while done < len(devices):
-            kind, dev, a, b = result_q.get()
-            if kind == "row":
-                chunks.append((a[0], a[1], a[2], b))
-            elif kind == "done":
-                done += 1
-                facts[dev] = a
-            else:
-                raise RuntimeError(f"sweep worker on device {dev} failed: {a}")
+        if pending:
+            for slot, dev in enumerate(devices):
+                spawn(slot, dev, 0)
+        while busy():
+            live = {s["conn"]: k for k, s in slots.items() if s["ready"] != "stopping"}
+            ready_conns = mp_connection.wait(list(live), timeout=poll_s)
+            for conn in ready_conns:
+                slot = live[conn]
+                if slot not in slots:
+                    continue
+                try:
+                    kind, dev_slot, task, payload = conn.recv()
+                except (EOFError, OSError):
+                    slots[slot]["proc"].join(timeout=10)  # reap it: exitcode is then set
+                    code = slots[slot]["proc"].exitcode
+                    fail_task(slot, f"worker exited with code {code} without reporting")
+                    continue
+                if kind == "ready":
+                    slots[slot]["ready"] = True
+                    facts.setdefault(dev_slot, payload)
+                    hand_out(slot)
+                elif kind == "row":
+                    row, clocks = payload
+                    chunks.append((task[0], task[1], task[2], row))
+                    entry = {"task": list(task), "device": dev_slot, "clocks": clocks}
+                    task_log.append(entry)
+                    if ckpt:
+                        ckpt.save(task, row, entry)
+                    hand_out(slot)
+                else:
+                    fail_task(slot, f"worker error: {payload}")
+            now = time.monotonic()
+            for slot in list(slots):
+                s = slots[slot]
+                if s["ready"] == "stopping":
+                    continue
+                code = s["proc"].exitcode
+                if code is not None and not s["conn"].poll():
+                    fail_task(slot, f"worker exited with code {code} without reporting")
+                elif not s["ready"] and now - s["started"] > start_timeout_s:
+                    fail_task(slot, "worker never became ready")
     finally:
-        for p in procs:
-            p.join(timeout=30)
-            if p.is_alive():
-                p.terminate()
+        for s in slots.values():
+            if s["ready"] != "stopping" and s["proc"].is_alive():
+                try:
+                    s["conn"].send(None)
+                except (OSError, ValueError):
+                    pass
+        for s in slots.values():
+            s["proc"].join(timeout=30)
+            if s["proc"].is_alive():
+                s["proc"].terminate()
     wall = time.perf_counter() - t0
     grid = merge_chunks(len(spec.problems), n_cfg, chunks)
     configs = tuple(spec.configs) if spec.configs is not None else gemm.family_configs(spec.family)
     first = facts[min(facts)] if facts else {}
-    return SweepResult(spec, configs, grid, wall, dict(first, devices=len(devices)))
+    return SweepResult(spec, configs, grid, wall, dict(first, devices=len(devices)),
+                       task_log=task_log)
 
 
 def sidecar(result: SweepResult, extra: dict | None = None) -> dict:
@@ -325,7 +514,12 @@ def sidecar(result: SweepResult, extra: dict | None = None) -> dict:
         "timing": "CUDA events on the launching stream (kp_sweep_problem)",
         "wall_s": result.wall_s, "cells_per_s": result.cells / result.wall_s,
         "device": result.device, "host_cores": os.cpu_count(),
+        "early_exit": "a config > 1 ms and > 8x the best median so far keeps its first timing "
+                      "(whole-problem tasks only; config-range tasks time every config fully)",
     }
+    if result.task_log:
+        # NVML SM clock + throttle reasons before/after every task
+        doc["task_clocks"] = result.task_log
     if extra:
         doc.update(extra)
     return doc

@@ -109,8 +109,12 @@ def test_plan_tasks_splits_only_dominant_problems_and_covers_every_cell():
     import numpy as np
     from paper_2003_06795_b200 import measure, shapes
     probs = shapes.problem_set("networks+squares")
-    assert measure.plan_tasks(probs, 1, 640) == [(i, 0, 640) for i in
-                                                 [t[0] for t in measure.plan_tasks(probs, 1, 640)]]
+    single = measure.plan_tasks(probs, 1, 640)
+    # one device: every problem exactly once, whole config range, longest first
+    assert sorted(i for i, _, _ in single) == list(range(len(probs)))
+    assert all((lo, hi) == (0, 640) for _, lo, hi in single)
+    single_costs = [measure.problem_cost(probs[i]) for i, _, _ in single]
+    assert single_costs == sorted(single_costs, reverse=True)
     for nd in (2, 4, 8):
         tasks = measure.plan_tasks(probs, nd, 640)
         cover = np.zeros((len(probs), 640), dtype=int)
@@ -140,3 +144,77 @@ def test_merge_chunks_contract():
     with pytest.raises(RuntimeError, match="non-positive"):
         measure.merge_chunks(1, 1, [(0, 0, 1, [0.0])])
     assert np.isfinite(grid).all()
+
+
+# ---- run_sharded robustness (fake workers, same protocol, no GPU) ----------
+
+def _fake_spec(n_problems=5, n_configs=7):
+    from paper_2003_06795_b200.dataset import KernelConfig
+    probs = tuple(ProblemSize(64 * (i + 1), 64, 64) for i in range(n_problems))
+    cfgs = tuple(KernelConfig(1, 1, 1, 8, 8) for _ in range(n_configs))
+    return measure.SweepSpec(probs, configs=cfgs)
+
+
+def _expected(spec):
+    import _fake_sweep_worker as fw
+    return np.array([[fw.cell(i, j) for j in range(len(spec.configs))]
+                     for i in range(len(spec.problems))])
+
+
+@pytest.fixture
+def fake_markers(tmp_path, monkeypatch):
+    import sys
+    sys.path.insert(0, os.path.dirname(__file__))
+    d = tmp_path / "markers"
+    d.mkdir()
+    monkeypatch.setenv("KP_FAKE_MARKERS", str(d))
+    yield d
+    sys.path.remove(os.path.dirname(__file__))
+
+
+def test_run_sharded_merges_every_task(fake_markers):
+    import _fake_sweep_worker as fw
+    spec = _fake_spec()
+    res = measure.run_sharded(spec, [0, 1], _worker_fn=fw.healthy, poll_s=0.2)
+    assert np.array_equal(res.runtime_ns, _expected(spec))
+    assert sorted(tuple(e["task"]) for e in res.task_log) == sorted(
+        measure.plan_tasks(spec.problems, 2, len(spec.configs)))
+
+
+def test_run_sharded_requeues_a_dead_workers_task(fake_markers):
+    """A worker that dies without a message is detected by the liveness poll,
+    its in-flight task re-runs on a restarted worker, and the grid is whole."""
+    import _fake_sweep_worker as fw
+    spec = _fake_spec()
+    res = measure.run_sharded(spec, [0, 1], _worker_fn=fw.crashes_once_on_problem_1,
+                              poll_s=0.2)
+    assert np.array_equal(res.runtime_ns, _expected(spec))
+    lost = [e for e in res.task_log if e.get("event") == "worker_lost"]
+    # problem 1 may be cut into config ranges: each range's first attempt dies once
+    assert lost and all(e["task"][0] == 1 and "code 9" in e["why"] for e in lost)
+
+
+def test_run_sharded_aborts_on_a_task_that_keeps_failing(fake_markers):
+    import _fake_sweep_worker as fw
+    spec = _fake_spec()
+    with pytest.raises(RuntimeError, match=r"task \(2, 0, 7\) failed 2 times"):
+        measure.run_sharded(spec, [0], _worker_fn=fw.always_fails_on_problem_2, poll_s=0.2)
+
+
+def test_run_sharded_resumes_from_task_shards(fake_markers, tmp_path):
+    import _fake_sweep_worker as fw
+    spec = _fake_spec()
+    ckpt = tmp_path / "ckpt"
+    with pytest.raises(RuntimeError):
+        measure.run_sharded(spec, [0], _worker_fn=fw.always_fails_on_problem_2, poll_s=0.2,
+                            checkpoint_dir=ckpt)
+    done_before = sorted(p.name for p in ckpt.glob("task_*.json"))
+    assert done_before and "task_p2_c0-7.json" not in done_before
+    res = measure.run_sharded(spec, [0], _worker_fn=fw.healthy, poll_s=0.2,
+                              checkpoint_dir=ckpt)
+    assert np.array_equal(res.runtime_ns, _expected(spec))
+    resumed = {tuple(e["task"]) for e in res.task_log if e.get("resumed")}
+    assert len(resumed) == len(done_before)
+    other = measure.SweepSpec(spec.problems[:2], configs=spec.configs)
+    with pytest.raises(RuntimeError, match="different sweep"):
+        measure.run_sharded(other, [0], _worker_fn=fw.healthy, checkpoint_dir=ckpt)

@@ -22,3 +22,13 @@ for fam in tf32 bf16; do
     run --tool memcheck python tools/run_config.py --family $fam --trans $t --cfg 2,1,2,8,8 --mkn 200,136,264 --iters 1 --no-time
   done
 done
+# persistent 1-CTA (NBUF = 2, double-buffered TMEM accumulator) and CTA-pair
+# kernels with several tiles per CTA / pair (round-2 parity gap)
+for tool in memcheck racecheck; do
+  for fam in tf32 bf16; do
+    run --tool $tool python tools/run_config.py --family $fam --trans nn --cfg 1,1,1,16,16 --mkn 1536,136,1536 --iters 1 --no-time
+    run --tool $tool python tools/run_config.py --family $fam --trans tn --cfg 4,1,4,16,16 --mkn 2200,72,2112 --iters 1 --no-time
+    run --tool $tool python tools/run_config.py --family $fam --trans nt --cfg 2,2,4,16,16 --mkn 4096,128,2048 --iters 1 --no-time
+    run --tool $tool python tools/run_config.py --family $fam --trans tt --cfg 4,2,8,16,16 --mkn 4096,96,4352 --iters 1 --no-time
+  done
+done
