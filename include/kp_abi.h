@@ -31,8 +31,8 @@
  *
  * Conventions: every entry point returns a status and never aborts; the
  * library allocates no device memory per call (TMEM is allocated/freed inside
- * the tcgen05 kernels; a 256 KB ring of stream-K hand-off flags is allocated
- * once per device on first use); calls are stream-ordered and reentrant; the message of
+ * the tcgen05 kernels; a 256 KB ring of stream-K hand-off flags and a 256 MB
+ * tcgen05 split-K workspace are allocated once per device on first use); calls are stream-ordered and reentrant; the message of
  * the last failure on the calling thread is available from kp_last_error().
  */
 #ifndef KP_ABI_H
@@ -139,6 +139,17 @@ kp_status kp_sweep_problem_ex(kp_family family, const kp_config* cfgs, int32_t n
  * stream-K whenever a problem has two or more tiles (tests).  Process-wide;
  * returns the previous mode, or -1 for an unknown mode (left unchanged). */
 int32_t   kp_set_schedule(int32_t mode);
+
+/* K2/K3 (tcgen05, 1-CTA configs) split-K.  0 = never; 1 (default) = auto:
+ * grids of output tiles filling under half the SMs cut each tile's K range
+ * into S contiguous ranges (one CTA each, >= 4 K stages per range, one wave
+ * of units), partial tiles go to a per-device workspace and a second kernel
+ * sums them in split order 0..S-1 (deterministic); n in
+ * [2, 64] = force n splits (clamped to the K stages; tests).  Process-wide;
+ * returns the previous mode, or -1 for an invalid mode (left unchanged).
+ * Replaces nothing in the reference (its GEMM is external):
+ * a scheduling policy inside the kernel family, not a config field. */
+int32_t   kp_set_tc_split(int32_t mode);
 
 /* ---- runtime selection (generated decision-tree header) --------------- */
 /* Config the compiled selector picks for (m,k,n); KP_ERR_UNSUPPORTED when no

@@ -32,7 +32,7 @@ EXPORTS = ("kp_abi_version", "kp_num_configs", "kp_config_at", "kp_config_valid"
            "kp_gemm", "kp_gemm_time", "kp_sweep_problem", "kp_select", "kp_gemm_auto",
            "kp_status_string", "kp_last_error", "kp_launch_count", "kp_device_info",
            "kp_fp32_peak", "kp_conv_output_shape", "kp_im2col", "kp_conv2d_auto",
-           "kp_set_schedule", "kp_sweep_problem_ex")
+           "kp_set_schedule", "kp_sweep_problem_ex", "kp_set_tc_split")
 
 
 class KpConfig(ctypes.Structure):
@@ -108,6 +108,7 @@ def _declare(lib):
         "kp_device_info": (c.c_int, [c.c_int32, P(c.c_int32), P(c.c_int32), P(c.c_int32)]),
         "kp_fp32_peak": (c.c_int, [P(c.c_double), c.c_void_p]),
         "kp_set_schedule": (c.c_int32, [c.c_int32]),
+        "kp_set_tc_split": (c.c_int32, [c.c_int32]),
         "kp_conv_output_shape": (c.c_int, [P(KpConvDesc), P(c.c_int64), P(c.c_int64)]),
         "kp_im2col": (c.c_int, [c.c_int, P(KpConvDesc), c.c_void_p, c.c_void_p, c.c_void_p]),
         "kp_conv2d_auto": (c.c_int, [c.c_int, P(KpConvDesc), c.c_void_p, c.c_void_p, c.c_void_p,

@@ -279,6 +279,8 @@ int32_t kp_set_schedule(int32_t mode) {
     return g_schedule.exchange(mode);
 }
 
+int32_t kp_set_tc_split(int32_t mode) { return tc::set_split_mode(mode); }
+
 kp_status kp_gemm(kp_family family, kp_config cfg, const kp_gemm_desc* desc, const void* A,
                   const void* B, float* C, void* stream) {
     kp_status st;

@@ -27,6 +27,18 @@
 //                        MMAs of tile i+1
 //   row_tile 2        -> CTA pair, cta_group::2, M = 256 (persistent, ct 4|8)
 // 40 configs per family, canonical KernelConfig order.
+//
+// Split-K (1-CTA kernels, kp_set_tc_split): when the output tiles fill less
+// than half of the SMs -- deep-K network GEMMs such as ResNet-50 c5_3x3 at
+// batch 8 (392 x 4608 x 512: 16 tiles of 128 x 128 on 148 SMs) -- each tile's
+// K range is cut into S contiguous k-tile ranges, one work unit each, and
+// every unit writes its fp32 partial tile to a per-device workspace. A second
+// kernel (tc_splitk_reduce, launched with programmatic dependent launch so its
+// launch overlaps the GEMM) sums the S partials of every element in split
+// order 0..S-1 -- fixed, so results are run-to-run deterministic -- applies
+// alpha / beta and writes C. (Reducing in the last-arriving unit instead
+// serialises S x 64-128 KB of L2 reads through one SM per tile: measured 2x
+// slower than no split at all on c5_3x3.)
 #include <cuda.h>
 
 #include <algorithm>
@@ -54,7 +66,15 @@ struct TcParams {
     int stages, k_tiles;
     int batch;
     int a_batch, b_batch;  // 1 if the operand advances with the batch index, else 0
+    int splits;            // K splits per tile (1 = no split-K)
+    float* ws;             // split-K partial tiles [tile][split][BM][BN] (splits > 1)
 };
+
+// k-tile range [kb0, kb1) of split s of S over k_tiles (never empty for S <= k_tiles)
+__device__ __forceinline__ void split_range(int s, int S, int k_tiles, int& kb0, int& kb1) {
+    kb0 = int((int64_t(s) * k_tiles) / S);
+    kb1 = int((int64_t(s + 1) * k_tiles) / S);
+}
 
 // ------------------------------------------------------------ PTX wrappers
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
@@ -233,7 +253,10 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const int total = p.tiles_m * p.tiles_n * p.batch;
+    const int units = p.tiles_m * p.tiles_n * p.batch * p.splits;  // (tile, K split) work units
+    // let the split-K reduce kernel's launch start now; its griddepcontrol.wait
+    // still waits for this whole grid to finish and flush
+    if (p.splits > 1) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < S; ++s) {
@@ -259,13 +282,14 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     const uint32_t tmem = *tmem_slot;
 
     if (warp == 0) {
-        if (lane == 0) {  // ---- TMA producer: one ring across all of this CTA's tiles
+        if (lane == 0) {  // ---- TMA producer: one ring across all of this CTA's units
             int kt_all = 0;
-            for (int t = blockIdx.x; t < total; t += gridDim.x) {
-                int m0, n0, bz;
-                tile_coords(t, p, BN, m0, n0, bz);
+            for (int u = blockIdx.x; u < units; u += gridDim.x) {
+                int m0, n0, bz, kb0, kb1;
+                tile_coords(u / p.splits, p, BN, m0, n0, bz);
+                split_range(u % p.splits, p.splits, p.k_tiles, kb0, kb1);
                 const int za = bz * p.a_batch, zb = bz * p.b_batch;
-                for (int kt = 0; kt < p.k_tiles; ++kt, ++kt_all) {
+                for (int kt = kb0; kt < kb1; ++kt, ++kt_all) {
                     const int s = kt_all % S;
                     const uint32_t phase = (kt_all / S) & 1;
                     mbar_wait(empty_bar(s), phase ^ 1);
@@ -295,13 +319,15 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     } else if (warp == 1) {
         if (lane == 0) {  // ---- MMA issuer
             int kt_all = 0, it = 0;
-            for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+            for (int u = blockIdx.x; u < units; u += gridDim.x, ++it) {
+                int kb0, kb1;
+                split_range(u % p.splits, p.splits, p.k_tiles, kb0, kb1);
                 const int buf = NBUF == 2 ? (it & 1) : 0;
                 const uint32_t use = NBUF == 2 ? ((it >> 1) & 1) : (it & 1);
                 mbar_wait(acc_empty(buf), use ^ 1);  // epilogue drained this buffer
                 fence_after_sync();
                 const uint32_t d = tmem + uint32_t(buf * BN);
-                for (int kt = 0; kt < p.k_tiles; ++kt, ++kt_all) {
+                for (int kt = kb0; kt < kb1; ++kt, ++kt_all) {
                     const int s = kt_all % S;
                     const uint32_t phase = (kt_all / S) & 1;
                     mbar_wait(full_bar(s), phase);
@@ -319,7 +345,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                         const uint64_t db =
                             B_MN ? smem_desc(sb + k * UMMA_K * MB::W, BK * MB::W, MB::SBO, MB::LAYOUT)
                                  : smem_desc(sb + k * 32, 16, 1024, 2);
-                        mma<ES>(d, da, db, IDESC, (kt | k) != 0);
+                        mma<ES>(d, da, db, IDESC, (kt != kb0) || (k != 0));
                     }
                     umma_commit(empty_bar(s));  // frees the stage once these MMAs retire
                 }
@@ -330,7 +356,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         const int q = warp & 3;
         float* st = staging + (warp - 2) * 32 * EPI_PITCH;
         int it = 0;
-        for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+        for (int u = blockIdx.x; u < units; u += gridDim.x, ++it) {
+            const int t = u / p.splits;
             int m0, n0, bz;
             tile_coords(t, p, BN, m0, n0, bz);
             const int buf = NBUF == 2 ? (it & 1) : 0;
@@ -341,6 +368,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             const int row0 = m0 + q * 32;
             const uint32_t taddr = tmem + (uint32_t(q * 32) << 16) + uint32_t(buf * BN);
             const int cols = min(BN, p.N - n0);
+            // split-K: this unit's partial tile, full BM x BN, row-major
+            float* part = p.splits > 1
+                ? p.ws + (int64_t(t) * p.splits + u % p.splits) * (BM * BN) : nullptr;
 #pragma unroll 1
             for (int c0 = 0; c0 < cols; c0 += 32) {
                 float v[32];
@@ -348,15 +378,21 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
 #pragma unroll
                 for (int j = 0; j < 32; ++j) st[lane * EPI_PITCH + j] = v[j];
                 __syncwarp();
-                const int n = n0 + c0 + lane;
-                if (n < p.N) {
+                if (part) {
 #pragma unroll 4
-                    for (int r = 0; r < 32; ++r) {
-                        const int m = row0 + r;
-                        if (m < p.M) {
-                            float* dst = Cb + int64_t(m) * p.ldc + n;
-                            const float x = p.alpha * st[r * EPI_PITCH + lane];
-                            *dst = p.beta == 0.0f ? x : fmaf(p.beta, *dst, x);
+                    for (int r = 0; r < 32; ++r)
+                        __stcg(part + (q * 32 + r) * BN + c0 + lane, st[r * EPI_PITCH + lane]);
+                } else {
+                    const int n = n0 + c0 + lane;
+                    if (n < p.N) {
+#pragma unroll 4
+                        for (int r = 0; r < 32; ++r) {
+                            const int m = row0 + r;
+                            if (m < p.M) {
+                                float* dst = Cb + int64_t(m) * p.ldc + n;
+                                const float x = p.alpha * st[r * EPI_PITCH + lane];
+                                *dst = p.beta == 0.0f ? x : fmaf(p.beta, *dst, x);
+                            }
                         }
                     }
                 }
@@ -375,6 +411,40 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         fence_after_sync();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem),
                      "r"(TMEM_COLS) : "memory");
+    }
+}
+
+// Split-K reduction: one thread per 4 consecutive columns of one tile row;
+// sums the S partials in split order, then alpha / beta and bounds.
+template <int BN>
+__global__ void __launch_bounds__(256)
+tc_splitk_reduce(const TcParams p) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // partials complete and visible
+    constexpr int C4 = BN / 4;                           // float4 columns per tile row
+    const int64_t total = int64_t(p.tiles_m) * p.tiles_n * p.batch * BM * C4;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const int c4 = int(i % C4);
+        const int r = int((i / C4) % BM);
+        const int t = int(i / (int64_t(C4) * BM));
+        int m0, n0, bz;
+        tile_coords(t, p, BN, m0, n0, bz);
+        const int m = m0 + r, n = n0 + 4 * c4;
+        if (m >= p.M || n >= p.N) continue;
+        const float4* src = reinterpret_cast<const float4*>(
+            p.ws + int64_t(t) * p.splits * (BM * BN) + r * BN) + c4;
+        float4 acc = __ldcg(src);
+        for (int sp = 1; sp < p.splits; ++sp) {
+            const float4 v = __ldcg(src + int64_t(sp) * (BM * BN / 4));
+            acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        }
+        float* dst = p.C + int64_t(bz) * p.sc + int64_t(m) * p.ldc + n;
+        const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
+        const int cols = min(4, p.N - n);
+        for (int j = 0; j < cols; ++j) {
+            const float x = p.alpha * a4[j];
+            dst[j] = p.beta == 0.0f ? x : fmaf(p.beta, dst[j], x);
+        }
     }
 }
 
@@ -707,6 +777,57 @@ static int sm_count() {
     return n;
 }
 
+// ---------------------------------------------------------- split-K state
+// Per-device workspace: WS_SLOTS slots of WS_SLOT_BYTES of partial tiles.
+// Launches take slots round-robin, so up to WS_SLOTS split-K GEMMs in flight
+// on different streams never share a slot.
+constexpr int WS_SLOTS = 4;
+constexpr size_t WS_SLOT_BYTES = size_t(64) << 20;
+static std::atomic<int> g_split_mode{1};
+
+int32_t set_split_mode(int32_t mode) {
+    if (mode < 0 || mode > 64) return -1;
+    return g_split_mode.exchange(mode);
+}
+
+static kp_status ws_reserve(float** ws) {
+    static std::mutex mu;
+    static char* base[64] = {nullptr};
+    static unsigned next[64] = {0};
+    const int dev = current_device();
+    if (dev < 0 || dev >= 64) return fail(KP_ERR_CUDA, "split-K: bad device");
+    std::lock_guard<std::mutex> lock(mu);
+    if (!base[dev]) {
+        void* ptr = nullptr;
+        if (cudaMalloc(&ptr, WS_SLOTS * WS_SLOT_BYTES) != cudaSuccess)
+            return check_launch("split-K workspace cudaMalloc");
+        base[dev] = static_cast<char*>(ptr);
+    }
+    *ws = reinterpret_cast<float*>(base[dev] + (next[dev]++ % WS_SLOTS) * WS_SLOT_BYTES);
+    return KP_OK;
+}
+
+// K splits for a grid of `tiles` 128 x bn tiles over k_tiles K stages.
+// Auto (mode 1): only grids filling under half the SMs split, into as many
+// ranges as one wave of units allows while every range keeps >= 4 k-tiles
+// (the TMA ring's fill must stay amortised); mode >= 2 forces that many
+// splits (tests); mode 0 never splits.
+static int choose_splits(int64_t tiles, int k_tiles, int bn) {
+    const int mode = g_split_mode.load(std::memory_order_relaxed);
+    if (mode == 0) return 1;
+    int64_t S;
+    if (mode >= 2) {
+        S = mode;
+    } else {
+        const int sms = sm_count();
+        if (tiles * 2 > sms) return 1;
+        S = std::min<int64_t>(sms / tiles, k_tiles / 4);
+    }
+    S = std::min<int64_t>(S, k_tiles);
+    S = std::min<int64_t>(S, int64_t(WS_SLOT_BYTES / (size_t(BM) * bn * sizeof(float))) / tiles);
+    return S < 2 ? 1 : int(S);
+}
+
 template <int ES, int BN, bool A_MN, bool B_MN, int NBUF>
 static kp_status launch_t(const GemmProblem& g, int want_stages, cudaStream_t stream) {
     int stages = want_stages;
@@ -748,10 +869,29 @@ static kp_status launch_t(const GemmProblem& g, int want_stages, cudaStream_t st
     p.b_batch = g.sb ? 1 : 0;
     const int64_t tiles = int64_t(p.tiles_m) * p.tiles_n * g.batch;
     if (tiles > 0x7fffffffLL) return fail(KP_ERR_BAD_SHAPE, "tc: grid too large");
-    const int64_t grid = NBUF == 2 ? std::min<int64_t>(tiles, sm_count()) : tiles;
+    p.splits = choose_splits(tiles, p.k_tiles, BN);
+    p.ws = nullptr;
+    if (p.splits > 1 && (st = ws_reserve(&p.ws)) != KP_OK) return st;
+    const int64_t units = tiles * p.splits;
+    const int64_t grid = NBUF == 2 ? std::min<int64_t>(units, sm_count()) : units;
     kern<<<dim3(unsigned(grid)), NUM_THREADS, smem, stream>>>(ma, mb, p);
     note_launch();
-    return check_launch("tc_gemm_kernel");
+    if ((st = check_launch("tc_gemm_kernel")) != KP_OK || p.splits == 1) return st;
+    // split-K: reduce the partials (programmatic dependent launch)
+    const int64_t work = tiles * BM * (BN / 4);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(std::min<int64_t>((work + 255) / 256, int64_t(sm_count()) * 8)));
+    cfg.blockDim = dim3(256);
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, tc_splitk_reduce<BN>, p) != cudaSuccess)
+        return check_launch("tc_splitk_reduce");
+    note_launch();
+    return check_launch("tc_splitk_reduce");
 }
 
 static size_t pair_smem_bytes(int bn, int stages) {
@@ -792,6 +932,8 @@ static kp_status launch_pair(const GemmProblem& g, int want_stages, cudaStream_t
     p.M = int(g.m); p.N = int(g.n); p.K = int(g.k);
     p.ldc = g.ldc; p.sc = g.sc;
     p.alpha = g.alpha; p.beta = g.beta;
+    p.splits = 1;  // the pair kernel never splits K
+    p.ws = nullptr;
     p.tiles_m = int((g.m + 2 * BM - 1) / (2 * BM));  // 256-row pair tiles
     p.tiles_n = int((g.n + BN - 1) / BN);
     p.stages = stages;

@@ -49,8 +49,8 @@ def _store(m, k, n, ta, tb, seed, dtype=torch.float32, pad_to=1):
 
     def mk(rows, cols):
         pitch = -(-cols // pad_to) * pad_to
-        t = torch.rand((rows, pitch), generator=g, device="cuda") * 2 - 1
-        return t[:, :cols].to(dtype)
+        t = (torch.rand((rows, pitch), generator=g, device="cuda") * 2 - 1).to(dtype)
+        return t[:, :cols]  # slice after the cast: .to() of a padded view would repack it
 
     a = mk(k, m) if ta else mk(m, k)
     b = mk(n, k) if tb else mk(k, n)
@@ -73,7 +73,7 @@ def test_f32_selected_bit_exact(name, ta, tb):
     a_sub = a_np[:, rows] if ta else a_np[rows]
     want = gemm_f32_exact(a_sub, b_np, m=len(rows), k=k, n=n, trans_a=ta,
                           trans_b=tb).reshape(len(rows), n)
-    np.testing.assert_array_equal(got[rows], want, err_msg=f"{name} {ta}{tb} {tuple(cfg)}")
+    np.testing.assert_array_equal(got[rows], want, err_msg=f"{name} {ta}{tb} {cfg.as_tuple()}")
 
 
 @pytest.mark.parametrize("family", ["tf32", "bf16"])

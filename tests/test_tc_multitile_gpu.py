@@ -89,7 +89,7 @@ def check_large(family, cfg, m, k, n, ta, tb, seed=0, rows_per_tile=5):
 MULTITILE = [
     ((1, 1, 1, 16, 16), 2048, 512, 2048),   # BN 32: 1024 tiles, ~7 per CTA
     ((4, 1, 2, 16, 16), 2048, 520, 2048),   # BN 64: 512 tiles, ragged K
-    ((8, 1, 4, 16, 16), 2176, 256, 2112),   # BN 128: 17 x 17 tiles, M/N tails
+    ((8, 1, 4, 16, 16), 2176, 256, 4160),   # BN 128: 17 x 33 tiles, M/N tails
     ((8, 1, 8, 16, 16), 4096, 256, 4096),   # BN 256: 512 tiles
     ((2, 2, 4, 16, 16), 4096, 256, 2048),   # pair BN 128: 256 pair tiles
     ((8, 2, 8, 16, 16), 4096, 264, 4352),   # pair BN 256: 272 pair tiles, N tail
@@ -136,4 +136,4 @@ def test_8192_cubed_sampled(family, cfg):
 @pytest.mark.parametrize("ta,tb", [(False, True), (True, False), (True, True)])
 def test_8192_cubed_layouts_selected(family, ta, tb):
     cfg = _gemm().select(8192, 8192, 8192, family=family, trans_a=ta, trans_b=tb)
-    check_large(family, tuple(cfg), 8192, 8192, 8192, ta, tb, seed=82, rows_per_tile=4)
+    check_large(family, cfg.as_tuple(), 8192, 8192, 8192, ta, tb, seed=82, rows_per_tile=4)

@@ -17,6 +17,7 @@ def main():
     ap.add_argument("--trans", default="nn")
     ap.add_argument("--iters", type=int, default=3)
     ap.add_argument("--schedule", type=int, help="K1 tile schedule (kp_set_schedule)")
+    ap.add_argument("--tc-split", type=int, help="tcgen05 split-K mode (kp_set_tc_split)")
     ap.add_argument("--no-time", action="store_true", help="launch only (sanitizer runs)")
     args = ap.parse_args()
     import torch
@@ -31,6 +32,9 @@ def main():
     if args.schedule is not None:
         from paper_2003_06795_b200 import _native as nat
         nat.lib().kp_set_schedule(args.schedule)
+    if args.tc_split is not None:
+        from paper_2003_06795_b200 import _native as nat
+        nat.lib().kp_set_tc_split(args.tc_split)
     for _ in range(args.iters):
         gemm.matmul(a, b, cfg, family=args.family)
     torch.cuda.synchronize()
