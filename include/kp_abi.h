@@ -26,6 +26,8 @@
  *   kp_select / kp_gemm_auto  <- generated `select_kernel(m,k,n)`,
  *                                codegen.py:128-171, compiled into the library
  *                                exactly as harness/parity_main.cpp:21-32,96 does
+ *   kp_gemm_skinny            <- no reference counterpart: small-M (FC layer)
+ *                                path behind kp_gemm_auto
  *   kp_status                 <- errors.py:4-9 DataError taxonomy; NonPositiveValue
  *                                (dataset.py:95-97) -> KP_ERR_BAD_SHAPE
  *
@@ -151,11 +153,38 @@ int32_t   kp_set_schedule(int32_t mode);
  * a scheduling policy inside the kernel family, not a config field. */
 int32_t   kp_set_tc_split(int32_t mode);
 
+/* ---- small-M path (m <= 16: fully connected layers at batch 1-16) ----- */
+/* A B-streaming kernel pair for any family (fp32 inputs for KP_F32_SIMT and
+ * KP_TF32_TC, bf16 for KP_BF16_TC; fp32 FMA accumulate): CTAs own a column
+ * block and a K range, stage op(A)'s m rows in shared memory and read B once
+ * with 16-byte loads; partial sums meet in a fixed order (warp order through
+ * shared memory for B normal, a warp-shuffle butterfly for B transposed,
+ * split order through a per-device workspace across K ranges), so results
+ * are deterministic but not in the sequential-fmaf order of K1.
+ * KP_ERR_UNSUPPORTED when m > 16.  kp_gemm / kp_gemm_time accept the
+ * all-zero config KP_SKINNY_CONFIG for the same path (timing, sweeps);
+ * kp_config_valid still rejects it (it is not a KernelConfig).
+ * Replaces nothing in the reference (its GEMM is external,
+ * PAPER.md:112-114): the FC-layer case of the paper's dataset
+ * that the tile configs cannot stream at HBM speed. */
+#define KP_SKINNY_CONFIG_INIT {0u, 0u, 0u, 0u, 0u}
+kp_status kp_gemm_skinny(kp_family family, const kp_gemm_desc* desc, const void* A,
+                         const void* B, float* C, void* stream);
+/* Whether kp_gemm_auto routes m <= 16 problems to the small-M path:
+ * 0 = never, 1 (default) = when k >= 64, n >= 64 and m <= 16 (KP_F32_SIMT)
+ * or m <= 4 (KP_TF32_TC / KP_BF16_TC), 2 = every m <= 16 problem.  kp_gemm_auto reports the all-zero config in `chosen`
+ * when it took this path.  Returns the previous mode, or -1 (unchanged). */
+int32_t   kp_set_skinny(int32_t mode);
+
 /* ---- runtime selection (generated decision-tree header) --------------- */
 /* Config the compiled selector picks for (m,k,n); KP_ERR_UNSUPPORTED when no
  * selector is compiled in for this family / transpose variant. */
 kp_status kp_select(kp_family family, int32_t trans_a, int32_t trans_b,
                     int64_t m, int64_t k, int64_t n, kp_config* out);
+/* What kp_gemm_auto launches for this shape: kp_select's config, or the
+ * all-zero config when the small-M path takes the problem. */
+kp_status kp_auto_config(kp_family family, int32_t trans_a, int32_t trans_b,
+                         int64_t m, int64_t k, int64_t n, kp_config* out);
 kp_status kp_gemm_auto(kp_family family, const kp_gemm_desc* desc,
                        const void* A, const void* B, float* C, void* stream,
                        kp_config* chosen /* may be NULL */);

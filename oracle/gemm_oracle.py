@@ -45,6 +45,8 @@ def _load():
         lib.kp_oracle_gemm_f32.restype = ctypes.c_int
         lib.kp_oracle_gemm_f32.argtypes = [i64, i64, i64, i64, i32, i32, i64, i64, i64,
                                            i64, i64, i64, f32, f32, vp, vp, vp]
+        lib.kp_oracle_set_threads.restype = ctypes.c_int
+        lib.kp_oracle_set_threads.argtypes = [ctypes.c_int]
         _lib = lib
     return _lib
 
@@ -70,6 +72,11 @@ def gemm_f32_exact(a_store: np.ndarray, b_store: np.ndarray, *, m: int, k: int, 
     if rc != 0:
         raise ValueError(f"oracle rejected the problem (rc={rc})")
     return c
+
+
+def set_threads(n: int) -> int:
+    """Host threads (OpenMP) the fmaf oracle uses; returns the previous count."""
+    return int(_load().kp_oracle_set_threads(int(n)))
 
 
 def gemm_f64(a: np.ndarray, b: np.ndarray) -> np.ndarray:

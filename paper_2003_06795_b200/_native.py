@@ -32,7 +32,8 @@ EXPORTS = ("kp_abi_version", "kp_num_configs", "kp_config_at", "kp_config_valid"
            "kp_gemm", "kp_gemm_time", "kp_sweep_problem", "kp_select", "kp_gemm_auto",
            "kp_status_string", "kp_last_error", "kp_launch_count", "kp_device_info",
            "kp_fp32_peak", "kp_conv_output_shape", "kp_im2col", "kp_conv2d_auto",
-           "kp_set_schedule", "kp_sweep_problem_ex", "kp_set_tc_split")
+           "kp_set_schedule", "kp_sweep_problem_ex", "kp_set_tc_split",
+           "kp_gemm_skinny", "kp_set_skinny", "kp_auto_config")
 
 
 class KpConfig(ctypes.Structure):
@@ -109,6 +110,11 @@ def _declare(lib):
         "kp_fp32_peak": (c.c_int, [P(c.c_double), c.c_void_p]),
         "kp_set_schedule": (c.c_int32, [c.c_int32]),
         "kp_set_tc_split": (c.c_int32, [c.c_int32]),
+        "kp_set_skinny": (c.c_int32, [c.c_int32]),
+        "kp_auto_config": (c.c_int, [c.c_int, c.c_int32, c.c_int32, c.c_int64, c.c_int64,
+                                     c.c_int64, P(KpConfig)]),
+        "kp_gemm_skinny": (c.c_int, [c.c_int, P(KpGemmDesc), c.c_void_p, c.c_void_p,
+                                     c.c_void_p, c.c_void_p]),
         "kp_conv_output_shape": (c.c_int, [P(KpConvDesc), P(c.c_int64), P(c.c_int64)]),
         "kp_im2col": (c.c_int, [c.c_int, P(KpConvDesc), c.c_void_p, c.c_void_p, c.c_void_p]),
         "kp_conv2d_auto": (c.c_int, [c.c_int, P(KpConvDesc), c.c_void_p, c.c_void_p, c.c_void_p,
@@ -166,6 +172,13 @@ def family_id(family) -> int:
         raise ValueError(f"unknown kernel family {family!r}, expected one of {tuple(FAMILIES)}")
 
 
+SKINNY = "skinny"  # the small-M path's config name (all-zero kp_config)
+
+
 def to_kp_config(cfg) -> KpConfig:
+    if isinstance(cfg, str):
+        if cfg != SKINNY:
+            raise ValueError(f"unknown config name {cfg!r}")
+        return KpConfig(0, 0, 0, 0, 0)
     t = cfg.as_tuple() if hasattr(cfg, "as_tuple") else tuple(cfg)
     return KpConfig(*[int(v) for v in t])

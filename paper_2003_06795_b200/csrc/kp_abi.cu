@@ -14,6 +14,7 @@
 #include "kp_internal.cuh"
 #include "simt_registry.h"
 #include "tc_registry.h"
+#include "skinny_registry.h"
 #include "generated/selectors.h"
 
 namespace kp {
@@ -164,7 +165,13 @@ static kp_status valid_config(kp_family fam, const kp_config& c) {
     return fail(KP_ERR_INVALID_ARG, "unknown kernel family");
 }
 
+// The all-zero config names the small-M path (KP_SKINNY_CONFIG in kp_abi.h).
+static bool is_skinny(const kp_config& c) {
+    return c.acc == 0 && c.row_tile == 0 && c.col_tile == 0 && c.wg_rows == 0 && c.wg_cols == 0;
+}
+
 static kp_status run(kp_family fam, const kp_config& c, const GemmProblem& g, cudaStream_t s) {
+    if (is_skinny(c)) return skinny::launch(fam, g, s);
     if (fam == KP_F32_SIMT) {
         const int layout = (g.ta ? 2 : 0) + (g.tb ? 1 : 0);
 #ifdef KP_LEAN
@@ -281,10 +288,20 @@ int32_t kp_set_schedule(int32_t mode) {
 
 int32_t kp_set_tc_split(int32_t mode) { return tc::set_split_mode(mode); }
 
+int32_t kp_set_skinny(int32_t mode) { return skinny::set_mode(mode); }
+
+kp_status kp_gemm_skinny(kp_family family, const kp_gemm_desc* desc, const void* A,
+                         const void* B, float* C, void* stream) {
+    kp_status st;
+    GemmProblem g;
+    if ((st = to_problem(desc, A, B, C, &g)) != KP_OK) return st;
+    return skinny::launch(family, g, static_cast<cudaStream_t>(stream));
+}
+
 kp_status kp_gemm(kp_family family, kp_config cfg, const kp_gemm_desc* desc, const void* A,
                   const void* B, float* C, void* stream) {
     kp_status st;
-    if ((st = valid_config(family, cfg)) != KP_OK) return st;
+    if (!is_skinny(cfg) && (st = valid_config(family, cfg)) != KP_OK) return st;
     GemmProblem g;
     if ((st = to_problem(desc, A, B, C, &g)) != KP_OK) return st;
     return run(family, cfg, g, static_cast<cudaStream_t>(stream));
@@ -295,7 +312,7 @@ kp_status kp_gemm_time(kp_family family, kp_config cfg, const kp_gemm_desc* desc
                        double max_cell_ns, double* runtime_ns, void* stream) {
     kp_status st;
     if (!runtime_ns) return fail(KP_ERR_INVALID_ARG, "null runtime output");
-    if ((st = valid_config(family, cfg)) != KP_OK) return st;
+    if (!is_skinny(cfg) && (st = valid_config(family, cfg)) != KP_OK) return st;
     GemmProblem g;
     if ((st = to_problem(desc, A, B, C, &g)) != KP_OK) return st;
     return time_one(family, cfg, g, warmup, reps, min_sample_ns, max_cell_ns, runtime_ns,
@@ -359,12 +376,29 @@ kp_status kp_select(kp_family family, int32_t trans_a, int32_t trans_b, int64_t 
     return fail(KP_ERR_UNSUPPORTED, "no selector compiled in for this family / transpose variant");
 }
 
+kp_status kp_auto_config(kp_family family, int32_t trans_a, int32_t trans_b, int64_t m, int64_t k,
+                         int64_t n, kp_config* out) {
+    if (!out) return fail(KP_ERR_INVALID_ARG, "null output");
+    kp_status st = kp_select(family, trans_a, trans_b, m, k, n, out);
+    if (st != KP_OK) return st;
+    GemmProblem g{};
+    g.batch = 1; g.m = m; g.k = k; g.n = n;
+    if (skinny::eligible(family, g)) *out = kp_config{0, 0, 0, 0, 0};
+    return KP_OK;
+}
+
 kp_status kp_gemm_auto(kp_family family, const kp_gemm_desc* desc, const void* A, const void* B,
                        float* C, void* stream, kp_config* chosen) {
     if (!desc) return fail(KP_ERR_INVALID_ARG, "null gemm descriptor");
     kp_config cfg;
     kp_status st = kp_select(family, desc->trans_a, desc->trans_b, desc->m, desc->k, desc->n, &cfg);
     if (st != KP_OK) return st;
+    GemmProblem g;
+    if ((st = to_problem(desc, A, B, C, &g)) != KP_OK) return st;
+    if (skinny::eligible(family, g)) {  // small-M (FC) shapes: the HBM-streaming path
+        if (chosen) *chosen = kp_config{0, 0, 0, 0, 0};
+        return skinny::launch(family, g, static_cast<cudaStream_t>(stream));
+    }
     if (chosen) *chosen = cfg;
     return kp_gemm(family, cfg, desc, A, B, C, stream);
 }

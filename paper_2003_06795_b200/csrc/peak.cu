@@ -3,22 +3,26 @@
 // Every thread runs 8 independent fma chains; a full-chip grid keeps all four
 // SMSPs of every SM issuing back to back.  Two forms, the larger one wins:
 // scalar FFMA with immediate operands (one register read per FMA) and the
-// packed FFMA2 (fp32x2) form K1's inner product uses.
+// packed FFMA2 (fp32x2) form K1's inner product uses.  The iteration count is
+// calibrated so every timed launch runs >= 12 ms: launch latency and the
+// ramp of the first and last waves stay below 0.1 % of the measurement.
 #include <algorithm>
+#include <cmath>
 
 #include "kp_internal.cuh"
 
 namespace kp {
 
 constexpr int kPeakChains = 8;
-constexpr int kPeakIters = 8192;
+constexpr int kPeakCalibIters = 8192;
+constexpr double kPeakMinMs = 12.0;
 
-__global__ void __launch_bounds__(256) ffma_peak_kernel(float* out, float seed) {
+__global__ void __launch_bounds__(256) ffma_peak_kernel(float* out, float seed, int iters) {
     float v[kPeakChains];
 #pragma unroll
     for (int c = 0; c < kPeakChains; ++c) v[c] = seed + threadIdx.x * 1e-7f + c;
     const float b = 0.999999f, a = 1e-7f;
-    for (int i = 0; i < kPeakIters; ++i) {
+    for (int i = 0; i < iters; ++i) {
 #pragma unroll
         for (int c = 0; c < kPeakChains; ++c) v[c] = fmaf(v[c], b, a);
     }
@@ -28,13 +32,13 @@ __global__ void __launch_bounds__(256) ffma_peak_kernel(float* out, float seed) 
     if (s == 123.456f) out[0] = s;  // keeps the chains live
 }
 
-__global__ void __launch_bounds__(256) ffma2_peak_kernel(float* out, float seed) {
+__global__ void __launch_bounds__(256) ffma2_peak_kernel(float* out, float seed, int iters) {
     float2 v[kPeakChains];
 #pragma unroll
     for (int c = 0; c < kPeakChains; ++c)
         v[c] = make_float2(seed + threadIdx.x * 1e-7f + c, seed - threadIdx.x * 1e-7f - c);
     const float2 b = make_float2(0.999999f, 0.999998f), a = make_float2(1e-7f, 2e-7f);
-    for (int i = 0; i < kPeakIters / 2; ++i) {
+    for (int i = 0; i < iters / 2; ++i) {
 #pragma unroll
         for (int c = 0; c < kPeakChains; ++c) v[c] = __ffma2_rn(v[c], b, a);
     }
@@ -59,20 +63,29 @@ extern "C" kp_status kp_fp32_peak(double* tflops, void* stream_) {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    double best = 0.0;
-    for (int rep = 0; rep < 12; ++rep) {
+    auto timed = [&](int form, int iters, float seed) {
         cudaEventRecord(e0, stream);
-        if (rep % 2 == 0)
-            ffma_peak_kernel<<<grid, block, 0, stream>>>(scratch, 1.0f + rep);
+        if (form == 0)
+            ffma_peak_kernel<<<grid, block, 0, stream>>>(scratch, seed, iters);
         else
-            ffma2_peak_kernel<<<grid, block, 0, stream>>>(scratch, 1.0f + rep);
+            ffma2_peak_kernel<<<grid, block, 0, stream>>>(scratch, seed, iters);
         note_launch();
         cudaEventRecord(e1, stream);
         cudaEventSynchronize(e1);
         float ms = 0.f;
         cudaEventElapsedTime(&ms, e0, e1);
-        const double flops = 2.0 * kPeakChains * kPeakIters * double(grid.x) * block.x;
-        if (rep > 1 && ms > 0.f) best = std::max(best, flops / (ms * 1e-3) / 1e12);
+        return double(ms);
+    };
+    // calibration: short launches (also the warm-up), then size for >= kPeakMinMs
+    double short_ms = 1e30;
+    for (int rep = 0; rep < 4; ++rep) short_ms = std::min(short_ms, timed(rep & 1, kPeakCalibIters, 1.0f + rep));
+    const double scale = std::max(1.0, std::ceil(kPeakMinMs / std::max(short_ms, 1e-3)));
+    const int iters = int(std::min(double(1 << 28), kPeakCalibIters * scale)) & ~1;
+    double best = 0.0;
+    for (int rep = 0; rep < 6; ++rep) {
+        const double ms = timed(rep & 1, iters, 2.0f + rep);
+        const double flops = 2.0 * kPeakChains * double(iters) * double(grid.x) * block.x;
+        if (ms > 0.0) best = std::max(best, flops / (ms * 1e-3) / 1e12);
     }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);

@@ -352,5 +352,23 @@ def select(m: int, k: int, n: int, *, family="f32", trans_a=False, trans_b=False
     return KernelConfig(*cfg.as_tuple())
 
 
+def auto_config(m: int, k: int, n: int, *, family="f32", trans_a=False, trans_b=False):
+    """What kp_gemm_auto runs for (m, k, n): the selector's KernelConfig, or
+    "skinny" when the small-M path (m <= 16) takes the problem."""
+    cfg = nat.KpConfig()
+    nat.check(nat.lib().kp_auto_config(nat.family_id(family), int(trans_a), int(trans_b), m, k,
+                                       n, ctypes.byref(cfg)), "kp_auto_config")
+    t = cfg.as_tuple()
+    return nat.SKINNY if t == (0, 0, 0, 0, 0) else KernelConfig(*t)
+
+
+def set_skinny(mode: int) -> int:
+    """kp_set_skinny: 0 never, 1 auto (default), 2 every m <= 16 problem."""
+    prev = int(nat.lib().kp_set_skinny(int(mode)))
+    if prev < 0:
+        raise ValueError(f"invalid skinny mode {mode}")
+    return prev
+
+
 def launch_count() -> int:
     return int(nat.lib().kp_launch_count())
