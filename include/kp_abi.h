@@ -32,7 +32,8 @@
  *                                (dataset.py:95-97) -> KP_ERR_BAD_SHAPE
  *
  * Conventions: every entry point returns a status and never aborts; the
- * library allocates no device memory per call (TMEM is allocated/freed inside
+ * library allocates no device memory per call except the stream-ordered
+ * staging copy of an unaligned tcgen05 operand (TMEM is allocated/freed inside
  * the tcgen05 kernels; a 256 KB ring of stream-K hand-off flags and a 256 MB
  * tcgen05 split-K workspace are allocated once per device on first use); calls are stream-ordered and reentrant; the message of
  * the last failure on the calling thread is available from kp_last_error().
@@ -96,6 +97,10 @@ kp_status kp_config_at(kp_family family, int32_t index, kp_config* out);
 kp_status kp_config_valid(kp_family family, kp_config cfg);
 
 /* ---- compute ----------------------------------------------------------- */
+/* The tcgen05 families load operands with TMA (16-byte aligned base, row and
+ * batch pitches).  An operand without that alignment is copied into a
+ * stream-ordered temporary (cudaMallocAsync / cudaFreeAsync on `stream`) with
+ * zero-padded 16-byte rows first; the result is the same GEMM. */
 kp_status kp_gemm(kp_family family, kp_config cfg, const kp_gemm_desc* desc,
                   const void* A, const void* B, float* C, void* stream);
 
@@ -193,7 +198,8 @@ kp_status kp_gemm_auto(kp_family family, const kp_gemm_desc* desc,
 /* NCHW input, weights [c_out, c_in*kh*kw] row-major, output NHWC
  * [batch*ho*wo, c_out]; the GEMM is the NT variant (kp_gemm_auto with
  * trans_b = 1), so conv layers run through the compiled NT selector.
- * Tensor-core families additionally need 16-byte aligned K pitches. */
+ * Tensor-core families: the im2col rows get a 16-byte K pitch (zero
+ * columns past K) and unaligned weights are staged (see kp_gemm). */
 typedef struct {
     int64_t batch, c_in, h, w, c_out, kh, kw, stride_h, stride_w, pad_h, pad_w;
 } kp_conv_desc;
@@ -201,6 +207,13 @@ kp_status kp_conv_output_shape(const kp_conv_desc* d, int64_t* ho, int64_t* wo);
 /* cols[batch*ho*wo, c_in*kh*kw] (fp32, bf16 for KP_BF16_TC), zero padding. */
 kp_status kp_im2col(kp_family family, const kp_conv_desc* d, const void* x, void* cols,
                     void* stream);
+/* Same gather with row pitch ldk >= c_in*kh*kw; columns [c_in*kh*kw, ldk)
+ * are written as zeros. */
+kp_status kp_im2col_pitched(kp_family family, const kp_conv_desc* d, const void* x, void* cols,
+                            int64_t ldk, void* stream);
+/* Elements of the `cols` workspace kp_conv2d_auto needs: batch*ho*wo rows of
+ * c_in*kh*kw, the pitch rounded up to 16 bytes for the tcgen05 families. */
+kp_status kp_conv_workspace_elems(kp_family family, const kp_conv_desc* d, int64_t* elems);
 kp_status kp_conv2d_auto(kp_family family, const kp_conv_desc* d, const void* x,
                          const void* w, float* y, void* cols /* workspace */, void* stream,
                          kp_config* chosen /* may be NULL */);

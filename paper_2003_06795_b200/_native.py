@@ -33,7 +33,8 @@ EXPORTS = ("kp_abi_version", "kp_num_configs", "kp_config_at", "kp_config_valid"
            "kp_status_string", "kp_last_error", "kp_launch_count", "kp_device_info",
            "kp_fp32_peak", "kp_conv_output_shape", "kp_im2col", "kp_conv2d_auto",
            "kp_set_schedule", "kp_sweep_problem_ex", "kp_set_tc_split",
-           "kp_gemm_skinny", "kp_set_skinny", "kp_auto_config")
+           "kp_gemm_skinny", "kp_set_skinny", "kp_auto_config", "kp_im2col_pitched",
+           "kp_conv_workspace_elems")
 
 
 class KpConfig(ctypes.Structure):
@@ -117,6 +118,9 @@ def _declare(lib):
                                      c.c_void_p, c.c_void_p]),
         "kp_conv_output_shape": (c.c_int, [P(KpConvDesc), P(c.c_int64), P(c.c_int64)]),
         "kp_im2col": (c.c_int, [c.c_int, P(KpConvDesc), c.c_void_p, c.c_void_p, c.c_void_p]),
+        "kp_im2col_pitched": (c.c_int, [c.c_int, P(KpConvDesc), c.c_void_p, c.c_void_p,
+                                        c.c_int64, c.c_void_p]),
+        "kp_conv_workspace_elems": (c.c_int, [c.c_int, P(KpConvDesc), P(c.c_int64)]),
         "kp_conv2d_auto": (c.c_int, [c.c_int, P(KpConvDesc), c.c_void_p, c.c_void_p, c.c_void_p,
                                      c.c_void_p, c.c_void_p, P(KpConfig)]),
     }

@@ -70,11 +70,14 @@ def conv2d(x, w, stride=1, padding=0, *, family="f32", nhwc: bool = False, works
     check_device(x, w, workspace)
     d = _desc(x, w, stride, padding)
     ho, wo = output_shape(x.shape, w.shape, stride, padding)
-    m, k = d.batch * ho * wo, d.c_in * d.kh * d.kw
+    k = d.c_in * d.kh * d.kw
     x = x.contiguous()
     wmat = w.reshape(d.c_out, k).contiguous()
-    if workspace is None or workspace.numel() < m * k or workspace.dtype != want:
-        workspace = torch.empty(m * k, dtype=want, device=x.device)
+    need = ctypes.c_int64()
+    nat.check(nat.lib().kp_conv_workspace_elems(fam, ctypes.byref(d), ctypes.byref(need)),
+              "kp_conv_workspace_elems")
+    if workspace is None or workspace.numel() < need.value or workspace.dtype != want:
+        workspace = torch.empty(need.value, dtype=want, device=x.device)
     y = torch.empty((d.batch, ho, wo, d.c_out), dtype=torch.float32, device=x.device)
     chosen = nat.KpConfig()
     with torch.cuda.device(x.device):

@@ -51,7 +51,8 @@ constexpr int kIm2colKC = 64;
 template <typename T, bool VEC>
 __global__ void __launch_bounds__(256) im2col_tiled_kernel(const T* __restrict__ x,
                                                            T* __restrict__ cols, Im2colGeom g,
-                                                           uint32_t rows, uint32_t K) {
+                                                           uint32_t rows, uint32_t K,
+                                                           uint32_t ldk) {
     constexpr int KC = kIm2colKC, PIX = kIm2colPix;
     __shared__ T tile[KC][PIX + 1];
     __shared__ int32_t tab_off[KC], tab_r[KC], tab_s[KC];
@@ -66,7 +67,9 @@ __global__ void __launch_bounds__(256) im2col_tiled_kernel(const T* __restrict__
     const int32_t ih0 = int32_t(oh) * g.stride_h - g.pad_h;
     const int32_t iw0 = int32_t(ow) * g.stride_w - g.pad_w;
     const T* xp = x + int64_t(b) * g.c_in * g.h * g.w + int64_t(ih0) * g.w + iw0;
-    for (uint32_t k0 = blockIdx.y * KC; k0 < K; k0 += gridDim.y * KC) {
+    // columns [K, ldk) of a padded pitch are written as zeros (taps past K
+    // gather nothing)
+    for (uint32_t k0 = blockIdx.y * KC; k0 < ldk; k0 += gridDim.y * KC) {
         if (t < KC && k0 + t < K) {
             const uint32_t k = k0 + t;
             const uint32_t c = g.khw.div(k);
@@ -105,11 +108,11 @@ __global__ void __launch_bounds__(256) im2col_tiled_kernel(const T* __restrict__
             for (int pass = 0; pass < PIX / RPP; ++pass) {
                 const int pr = t / LPR + pass * RPP;
                 const uint32_t row = row0 + pr;
-                if (row < rows && kk < K) {
+                if (row < rows && kk < ldk) {
                     union { uint4 u; T e[VW]; } out;
 #pragma unroll
                     for (int e = 0; e < VW; ++e) out.e[e] = tile[q * VW + e][pr];
-                    *reinterpret_cast<uint4*>(cols + int64_t(row) * K + kk) = out.u;
+                    *reinterpret_cast<uint4*>(cols + int64_t(row) * ldk + kk) = out.u;
                 }
             }
         } else {
@@ -117,7 +120,7 @@ __global__ void __launch_bounds__(256) im2col_tiled_kernel(const T* __restrict__
             for (int idx = t; idx < PIX * KC; idx += 256) {
                 const int pr = idx / KC, j = idx % KC;
                 const uint32_t row = row0 + pr;
-                if (row < rows && k0 + j < K) cols[int64_t(row) * K + k0 + j] = tile[j][pr];
+                if (row < rows && k0 + j < ldk) cols[int64_t(row) * ldk + k0 + j] = tile[j][pr];
             }
         }
         __syncthreads();
@@ -126,13 +129,13 @@ __global__ void __launch_bounds__(256) im2col_tiled_kernel(const T* __restrict__
 
 template <typename T, bool VEC>
 static void launch_im2col_tiled(const T* x, T* cols, const Im2colGeom& g, int64_t rows,
-                                int64_t K, int sms, cudaStream_t s) {
+                                int64_t K, int64_t ldk, int sms, cudaStream_t s) {
     const int64_t gx = (rows + kIm2colPix - 1) / kIm2colPix;
-    const int64_t kchunks = (K + kIm2colKC - 1) / kIm2colKC;
+    const int64_t kchunks = (ldk + kIm2colKC - 1) / kIm2colKC;
     const int64_t gy = std::min<int64_t>(
         std::min<int64_t>(kchunks, 65535), std::max<int64_t>(1, (int64_t(sms) * 8 + gx - 1) / gx));
     im2col_tiled_kernel<T, VEC><<<dim3(unsigned(gx), unsigned(gy)), 256, 0, s>>>(
-        x, cols, g, uint32_t(rows), uint32_t(K));
+        x, cols, g, uint32_t(rows), uint32_t(K), uint32_t(ldk));
     note_launch();
 }
 
@@ -156,18 +159,28 @@ extern "C" kp_status kp_conv_output_shape(const kp_conv_desc* d, int64_t* ho, in
     return conv_shape(d, ho, wo);
 }
 
-extern "C" kp_status kp_im2col(kp_family family, const kp_conv_desc* d, const void* x, void* cols,
-                               void* stream) {
+// K pitch of the im2col matrix kp_conv2d_auto uses: K itself, rounded up to
+// 16 bytes for the tcgen05 families (TMA needs 16-byte row pitches; the
+// padding columns are zeros and the GEMM still sees k = K).
+static int64_t conv_pitch(kp_family family, int64_t K) {
+    if (family == KP_TF32_TC) return (K + 3) / 4 * 4;
+    if (family == KP_BF16_TC) return (K + 7) / 8 * 8;
+    return K;
+}
+
+extern "C" kp_status kp_im2col_pitched(kp_family family, const kp_conv_desc* d, const void* x,
+                                       void* cols, int64_t ldk, void* stream) {
     int64_t ho, wo;
     kp_status st = conv_shape(d, &ho, &wo);
     if (st != KP_OK) return st;
     if (!x || !cols) return fail(KP_ERR_INVALID_ARG, "null tensor");
     const int64_t K = d->c_in * d->kh * d->kw, hwo = ho * wo;
-    if (K >= (1ll << 30) || hwo >= (1ll << 30) || d->c_in * d->h * d->w >= (1ll << 31))
+    if (ldk < K) return fail(KP_ERR_BAD_SHAPE, "im2col pitch smaller than c_in*kh*kw");
+    if (ldk >= (1ll << 30) || hwo >= (1ll << 30) || d->c_in * d->h * d->w >= (1ll << 31))
         return fail(KP_ERR_BAD_SHAPE, "conv dims exceed the 2^31 gather range");
     const bool bf16 = family == KP_BF16_TC;
     const int esz = bf16 ? 2 : 4;
-    const bool vec = K % (16 / esz) == 0 && aligned16(cols);
+    const bool vec = ldk % (16 / esz) == 0 && aligned16(cols);
     Im2colGeom g;
     g.hwo = FastDiv(uint32_t(hwo));
     g.wo = FastDiv(uint32_t(wo));
@@ -184,20 +197,36 @@ extern "C" kp_status kp_im2col(kp_family family, const kp_conv_desc* d, const vo
     const int64_t imgs = std::max<int64_t>(1, ((1ll << 31) - 2 * kIm2colPix) / hwo);
     for (int64_t b0 = 0; b0 < d->batch; b0 += imgs) {
         const int64_t nb = std::min(imgs, d->batch - b0);
-        const int64_t xoff = b0 * d->c_in * d->h * d->w, coff = b0 * hwo * K;
+        const int64_t xoff = b0 * d->c_in * d->h * d->w, coff = b0 * hwo * ldk;
         if (bf16) {
             auto xp = static_cast<const __nv_bfloat16*>(x) + xoff;
             auto cp = static_cast<__nv_bfloat16*>(cols) + coff;
-            if (vec) launch_im2col_tiled<__nv_bfloat16, true>(xp, cp, g, nb * hwo, K, sms, s);
-            else launch_im2col_tiled<__nv_bfloat16, false>(xp, cp, g, nb * hwo, K, sms, s);
+            if (vec) launch_im2col_tiled<__nv_bfloat16, true>(xp, cp, g, nb * hwo, K, ldk, sms, s);
+            else launch_im2col_tiled<__nv_bfloat16, false>(xp, cp, g, nb * hwo, K, ldk, sms, s);
         } else {
             auto xp = static_cast<const float*>(x) + xoff;
             auto cp = static_cast<float*>(cols) + coff;
-            if (vec) launch_im2col_tiled<float, true>(xp, cp, g, nb * hwo, K, sms, s);
-            else launch_im2col_tiled<float, false>(xp, cp, g, nb * hwo, K, sms, s);
+            if (vec) launch_im2col_tiled<float, true>(xp, cp, g, nb * hwo, K, ldk, sms, s);
+            else launch_im2col_tiled<float, false>(xp, cp, g, nb * hwo, K, ldk, sms, s);
         }
         if ((st = check_launch("im2col_kernel")) != KP_OK) return st;
     }
+    return KP_OK;
+}
+
+extern "C" kp_status kp_im2col(kp_family family, const kp_conv_desc* d, const void* x, void* cols,
+                               void* stream) {
+    if (!d) return fail(KP_ERR_INVALID_ARG, "null conv descriptor");
+    return kp_im2col_pitched(family, d, x, cols, d->c_in * d->kh * d->kw, stream);
+}
+
+extern "C" kp_status kp_conv_workspace_elems(kp_family family, const kp_conv_desc* d,
+                                             int64_t* elems) {
+    int64_t ho, wo;
+    if (!elems) return fail(KP_ERR_INVALID_ARG, "null output");
+    kp_status st = conv_shape(d, &ho, &wo);
+    if (st != KP_OK) return st;
+    *elems = d->batch * ho * wo * conv_pitch(family, d->c_in * d->kh * d->kw);
     return KP_OK;
 }
 
@@ -207,8 +236,10 @@ extern "C" kp_status kp_conv2d_auto(kp_family family, const kp_conv_desc* d, con
     int64_t ho, wo;
     kp_status st = conv_shape(d, &ho, &wo);
     if (st != KP_OK) return st;
-    if ((st = kp_im2col(family, d, x, cols, stream)) != KP_OK) return st;
     const int64_t m = d->batch * ho * wo, k = d->c_in * d->kh * d->kw, n = d->c_out;
-    kp_gemm_desc g = {1, m, k, n, 0, 1, k, k, n, 0, 0, m * n, 1.0f, 0.0f};
+    const int64_t ldk = conv_pitch(family, k);
+    if ((st = kp_im2col_pitched(family, d, x, cols, ldk, stream)) != KP_OK) return st;
+    // the weights' K pitch may still be unaligned: tc::launch stages them
+    kp_gemm_desc g = {1, m, k, n, 0, 1, ldk, k, n, 0, 0, m * n, 1.0f, 0.0f};
     return kp_gemm_auto(family, &g, cols, w, y, stream, chosen);
 }

@@ -40,6 +40,7 @@
 // serialises S x 64-128 KB of L2 reads through one SM per tile: measured 2x
 // slower than no split at all on c5_3x3.)
 #include <cuda.h>
+#include <cuda_bf16.h>
 
 #include <algorithm>
 #include <atomic>
@@ -1000,6 +1001,59 @@ static kp_status by_tile(const kp_config& c, const GemmProblem& g, cudaStream_t 
     return fail(KP_ERR_INVALID_CONFIG, "tc: bad col_tile");
 }
 
+// ------------------------------------------------ unaligned-operand staging
+// TMA needs 16-byte aligned bases and row / batch pitches.  An operand that
+// has neither (K = 27 im2col rows, odd leading dimensions, offset views) is
+// copied into a stream-ordered temporary (cudaMallocAsync from the device's
+// default pool, freed with cudaFreeAsync after the GEMM) whose rows are padded
+// to 16 bytes with zeros; the GEMM then runs on the copy with the same
+// logical shape, so only the staging bytes are extra.
+template <typename T>
+__global__ void __launch_bounds__(256)
+stage_rows_kernel(const T* __restrict__ src, T* __restrict__ dst, int64_t rows, int64_t cols,
+                  int64_t ld, int64_t bstride, int64_t ld_dst, int64_t batch) {
+    const int64_t per = rows * ld_dst, total = per * batch;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t b = i / per, e = i - b * per;
+        const int64_t r = e / ld_dst, c = e - r * ld_dst;
+        dst[i] = c < cols ? src[b * bstride + r * ld + c] : T(0.0f);
+    }
+}
+
+static kp_status stage_operand(bool bf16, const void* src, int64_t rows, int64_t cols, int64_t ld,
+                               int64_t bstride, int64_t batch, cudaStream_t s, void** out,
+                               int64_t* ld_out, int64_t* bstride_out) {
+    const int es = bf16 ? 2 : 4;
+    const int64_t ld2 = (cols + 16 / es - 1) / (16 / es) * (16 / es);
+    const int64_t bat = bstride ? batch : 1;  // a broadcast operand is staged once
+    const size_t bytes = size_t(bat) * rows * ld2 * es;
+    static std::once_flag pool_once[64];
+    const int dev = current_device();
+    std::call_once(pool_once[dev & 63], [dev] {  // keep freed staging memory pooled
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = ~uint64_t(0);
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+    });
+    if (cudaMallocAsync(out, bytes, s) != cudaSuccess) return check_launch("tc staging cudaMallocAsync");
+    const int64_t total = int64_t(bat) * rows * ld2;
+    const unsigned grid = unsigned(std::min<int64_t>((total + 255) / 256, int64_t(sm_count()) * 16));
+    if (bf16)
+        stage_rows_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(
+            static_cast<const __nv_bfloat16*>(src), static_cast<__nv_bfloat16*>(*out), rows, cols,
+            ld, bstride, ld2, bat);
+    else
+        stage_rows_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(src),
+                                                      static_cast<float*>(*out), rows, cols, ld,
+                                                      bstride, ld2, bat);
+    note_launch();
+    *ld_out = ld2;
+    *bstride_out = bstride ? rows * ld2 : 0;
+    return check_launch("stage_rows_kernel");
+}
+
 kp_status launch(kp_family fam, const kp_config& c, const GemmProblem& g, cudaStream_t s) {
     kp_status st = valid(fam, c);
     if (st != KP_OK) return st;
@@ -1007,9 +1061,24 @@ kp_status launch(kp_family fam, const kp_config& c, const GemmProblem& g, cudaSt
     auto al = [&](const void* ptr, int64_t ld, int64_t bs) {
         return aligned16(ptr) && (ld * es) % 16 == 0 && (g.batch == 1 || (bs * es) % 16 == 0);
     };
-    if (!al(g.A, g.lda, g.sa) || !al(g.B, g.ldb, g.sb))
-        return fail(KP_ERR_ALIGNMENT,
-                    "tcgen05 families need 16-byte aligned operands and row/batch pitches");
+    const bool a_ok = al(g.A, g.lda, g.sa), b_ok = al(g.B, g.ldb, g.sb);
+    if (!a_ok || !b_ok) {
+        GemmProblem h = g;
+        void* tmp[2] = {nullptr, nullptr};
+        const bool bf16 = fam == KP_BF16_TC;
+        if (!a_ok)
+            st = stage_operand(bf16, g.A, g.ta ? g.k : g.m, g.ta ? g.m : g.k, g.lda, g.sa, g.batch,
+                               s, &tmp[0], &h.lda, &h.sa);
+        if (st == KP_OK && !b_ok)
+            st = stage_operand(bf16, g.B, g.tb ? g.n : g.k, g.tb ? g.k : g.n, g.ldb, g.sb, g.batch,
+                               s, &tmp[1], &h.ldb, &h.sb);
+        if (tmp[0]) h.A = tmp[0];
+        if (tmp[1]) h.B = tmp[1];
+        if (st == KP_OK) st = launch(fam, c, h, s);
+        for (void* t : tmp)
+            if (t) cudaFreeAsync(t, s);
+        return st;
+    }
     if (c.row_tile == 2) return fam == KP_BF16_TC ? by_tile_pair<2>(c, g, s) : by_tile_pair<4>(c, g, s);
     const bool persistent = c.wg_rows == 16;
     if (fam == KP_BF16_TC) return persistent ? by_tile<2, 2>(c, g, s) : by_tile<2, 1>(c, g, s);

@@ -89,3 +89,34 @@ def test_conv2d_tensor_core(family):
     bound = 2.0 * 144 * u * torch.nn.functional.conv2d(x.double().cpu().abs(),
                                                        wt.double().cpu().abs(), padding=1)
     assert bool(((got - ref).abs() <= bound + 1e-30).all())
+
+
+@pytest.mark.parametrize("family", ["tf32", "bf16"])
+@pytest.mark.parametrize("layer", [(2, 3, 32, 32, 64, 3, 3, 1, 1),     # VGG conv1_1: K = 27
+                                   (2, 3, 64, 64, 64, 7, 7, 2, 3)])    # ResNet conv1: K = 147
+def test_conv2d_tensor_core_unaligned_k(family, layer):
+    """First layers whose K = Cin*kh*kw is not a 16-byte multiple: the im2col
+    rows get a padded pitch (zero columns) and the weights are staged."""
+    from paper_2003_06795_b200 import _native as nat, conv
+    import ctypes
+    b, c, h, w, co, kh, kw, st, pad = layer
+    rng = np.random.default_rng(5)
+    dt = torch.bfloat16 if family == "bf16" else torch.float32
+    x = torch.from_numpy(rng.uniform(-1, 1, (b, c, h, w)).astype(np.float32)).cuda().to(dt)
+    wt = torch.from_numpy(rng.uniform(-1, 1, (co, c, kh, kw)).astype(np.float32)).cuda().to(dt)
+    got = conv.conv2d(x, wt, st, pad, family=family).double().cpu()
+    ref = torch.nn.functional.conv2d(x.double().cpu(), wt.double().cpu(), stride=st, padding=pad)
+    u = 2.0 ** -10 if family == "tf32" else 2.0 ** -8
+    k = c * kh * kw
+    bound = 2.0 * k * u * torch.nn.functional.conv2d(x.double().cpu().abs(),
+                                                     wt.double().cpu().abs(), stride=st,
+                                                     padding=pad)
+    assert bool(((got - ref).abs() <= bound + 1e-30).all())
+    # the workspace query reports the padded pitch
+    d = conv._desc(x, wt, st, pad)
+    need = ctypes.c_int64()
+    nat.check(nat.lib().kp_conv_workspace_elems(nat.family_id(family), ctypes.byref(d),
+                                                ctypes.byref(need)))
+    al = 4 if family == "tf32" else 8
+    ho, wo = conv.output_shape(x.shape, wt.shape, st, pad)
+    assert need.value == b * ho * wo * (-(-k // al) * al)

@@ -171,6 +171,7 @@ import json, sys, numpy as np, torch
 sys.path.insert(0, sys.argv[1])
 from paper_2003_06795_b200 import gemm
 from oracle.gemm_oracle import gemm_f32_exact
+gemm.set_skinny(0)  # the tile selector's choice (the small-M path has its own tests)
 out = []
 for (m, k, n) in [(17, 27, 15), (200, 576, 64), (1, 4096, 1000), (512, 512, 512)]:
     rng = np.random.default_rng(m + k + n)

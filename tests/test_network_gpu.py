@@ -66,7 +66,7 @@ def test_f32_selected_bit_exact(name, ta, tb):
     la = a.t() if ta else a
     lb = b.t() if tb else b
     cfg = gemm.select(m, k, n, family="f32", trans_a=ta, trans_b=tb)
-    got = gemm.matmul(la, lb).cpu().numpy()
+    got = gemm.matmul(la, lb, cfg).cpu().numpy()  # the tree's tile config
     rows = _rows(m, seed=m + k)
     a_np = a.cpu().numpy()
     b_np = b.cpu().numpy()
@@ -74,6 +74,14 @@ def test_f32_selected_bit_exact(name, ta, tb):
     want = gemm_f32_exact(a_sub, b_np, m=len(rows), k=k, n=n, trans_a=ta,
                           trans_b=tb).reshape(len(rows), n)
     np.testing.assert_array_equal(got[rows], want, err_msg=f"{name} {ta}{tb} {cfg.as_tuple()}")
+    if gemm.auto_config(m, k, n, family="f32", trans_a=ta, trans_b=tb) == "skinny":
+        # kp_gemm_auto runs the small-M path here: fp64 oracle within the bound
+        auto = gemm.matmul(la, lb).double().cpu().numpy()
+        an = (a_np.T if ta else a_np).astype(np.float64)
+        ref = an @ (b_np.T if tb else b_np).astype(np.float64)
+        bound = 4.0 * k * 2.0 ** -24 * (np.abs(an) @ np.abs((b_np.T if tb else b_np)
+                                                           .astype(np.float64))) + 1e-30
+        assert (np.abs(auto - ref) <= bound).all(), name
 
 
 @pytest.mark.parametrize("family", ["tf32", "bf16"])

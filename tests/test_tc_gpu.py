@@ -73,12 +73,48 @@ def test_batched(family):
     _check(family, (2, 1, 8, 8, 8), 96, 72, 136, True, True, batch=2, seed=12)
 
 
-def test_alignment_error():
-    from paper_2003_06795_b200 import _native as nat
-    a = torch.ones(64, 27, device="cuda")   # row pitch 108 B: not 16-byte aligned
-    b = torch.ones(27, 64, device="cuda")
-    with pytest.raises(nat.BadProblemShape):
-        _gemm().matmul(a, b, (1, 1, 1, 8, 8), family="tf32")
+def _check_views(family, cfg, la, lb):
+    """Run on (possibly unaligned) views and compare with fp64."""
+    got = _gemm().matmul(la, lb, cfg, family=family).cpu().numpy().astype(np.float64)
+    an = la.float().cpu().numpy().astype(np.float64)
+    bn = lb.float().cpu().numpy().astype(np.float64)
+    k = an.shape[-1]
+    ref = np.matmul(an, bn)
+    bound = 2.0 * k * U[family] * np.matmul(np.abs(an), np.abs(bn)) + 1e-30
+    assert (np.abs(got - ref) <= bound).all(), (family, cfg, la.shape, lb.shape)
+
+
+@pytest.mark.parametrize("family", ["bf16", "tf32"])
+@pytest.mark.parametrize("ta,tb", [(False, False), (False, True), (True, False), (True, True)])
+@pytest.mark.parametrize("cfg", [(1, 1, 1, 8, 8), (4, 1, 4, 16, 16), (2, 2, 4, 16, 16)])
+def test_unaligned_operands_are_staged(family, ta, tb, cfg):
+    """Row pitches that are not 16-byte multiples (K = 27, the VGG conv1_1
+    im2col width; odd M / N pitches) and a misaligned base run through the
+    stream-ordered padded staging copy instead of failing."""
+    g = torch.Generator(device="cuda").manual_seed(3)
+    dt = torch.bfloat16 if family == "bf16" else torch.float32
+    m, k, n = 300, 27, 77
+    a = (torch.rand((k, m) if ta else (m, k), generator=g, device="cuda") * 2 - 1).to(dt)
+    b = (torch.rand((n, k) if tb else (k, n), generator=g, device="cuda") * 2 - 1).to(dt)
+    _check_views(family, cfg, a.t() if ta else a, b.t() if tb else b)
+    # misaligned base: a view starting one element into its storage
+    big = (torch.rand(m * k + 1, generator=g, device="cuda") * 2 - 1).to(dt)
+    a2 = big[1:].view(m, k)
+    _check_views(family, cfg, a2, b.t() if tb else b)
+
+
+@pytest.mark.parametrize("family", ["bf16", "tf32"])
+def test_unaligned_batched_and_broadcast(family):
+    g = torch.Generator(device="cuda").manual_seed(4)
+    dt = torch.bfloat16 if family == "bf16" else torch.float32
+    a = (torch.rand((3, 130, 147), generator=g, device="cuda") * 2 - 1).to(dt)  # ResNet conv1 K
+    b = (torch.rand((147, 65), generator=g, device="cuda") * 2 - 1).to(dt)     # broadcast B
+    got = _gemm().matmul(a, b, (2, 1, 2, 8, 8), family=family).cpu().double()
+    for i in range(3):
+        an = a[i].float().cpu().double()
+        ref = an @ b.float().cpu().double()
+        bound = 2.0 * 147 * U[family] * (an.abs() @ b.float().cpu().double().abs()) + 1e-30
+        assert bool(((got[i] - ref).abs() <= bound).all())
 
 
 @pytest.mark.parametrize("family", ["bf16", "tf32"])
