@@ -44,6 +44,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -54,7 +55,7 @@ namespace tc {
 
 constexpr int BM = 128;
 constexpr int NUM_THREADS = 192;
-constexpr int GROUP_M = 8;
+constexpr int GROUP_M = 8;  // default raster group (tc_group_m())
 constexpr int STAGE_ALIGN = 1024;
 constexpr int EPI_PITCH = 33;  // padded 32x32 staging tile per epilogue warp
 
@@ -68,6 +69,7 @@ struct TcParams {
     int batch;
     int a_batch, b_batch;  // 1 if the operand advances with the batch index, else 0
     int splits;            // K splits per tile (1 = no split-K)
+    int group_m;           // m-tiles per raster group
     float* ws;             // split-K partial tiles [tile][split][BM][BN] (splits > 1)
 };
 
@@ -209,10 +211,10 @@ __device__ __forceinline__ void tile_coords(int t, const TcParams& p, int bn, in
     const int per_batch = p.tiles_m * p.tiles_n;
     bz = t / per_batch;
     const int tile = t - bz * per_batch;
-    const int per_group = GROUP_M * p.tiles_n;
+    const int per_group = p.group_m * p.tiles_n;
     const int group = tile / per_group;
-    const int first_m = group * GROUP_M;
-    const int gsz = min(p.tiles_m - first_m, GROUP_M);
+    const int first_m = group * p.group_m;
+    const int gsz = min(p.tiles_m - first_m, p.group_m);
     const int in_group = tile - group * per_group;
     m0 = (first_m + in_group % gsz) * BM;
     n0 = (in_group / gsz) * bn;
@@ -779,6 +781,17 @@ static int sm_count() {
     return n;
 }
 
+// Raster group height (m-tiles sharing one sweep over n).  KP_TC_GROUP_M
+// overrides it for tuning experiments only (never set by the library).
+static int group_m() {
+    static const int g = [] {
+        const char* e = std::getenv("KP_TC_GROUP_M");
+        const int v = e ? std::atoi(e) : 0;
+        return v > 0 ? v : GROUP_M;
+    }();
+    return g;
+}
+
 // ---------------------------------------------------------- split-K state
 // Per-device workspace: WS_SLOTS slots of WS_SLOT_BYTES of partial tiles.
 // Launches take slots round-robin, so up to WS_SLOTS split-K GEMMs in flight
@@ -872,6 +885,7 @@ static kp_status launch_t(const GemmProblem& g, int want_stages, cudaStream_t st
     const int64_t tiles = int64_t(p.tiles_m) * p.tiles_n * g.batch;
     if (tiles > 0x7fffffffLL) return fail(KP_ERR_BAD_SHAPE, "tc: grid too large");
     p.splits = choose_splits(tiles, p.k_tiles, BN);
+    p.group_m = group_m();
     p.ws = nullptr;
     if (p.splits > 1 && (st = ws_reserve(&p.ws)) != KP_OK) return st;
     const int64_t units = tiles * p.splits;
@@ -935,6 +949,7 @@ static kp_status launch_pair(const GemmProblem& g, int want_stages, cudaStream_t
     p.ldc = g.ldc; p.sc = g.sc;
     p.alpha = g.alpha; p.beta = g.beta;
     p.splits = 1;  // the pair kernel never splits K
+    p.group_m = group_m();
     p.ws = nullptr;
     p.tiles_m = int((g.m + 2 * BM - 1) / (2 * BM));  // 256-row pair tiles
     p.tiles_n = int((g.n + BN - 1) / BN);
@@ -963,12 +978,38 @@ static kp_status launch_pair(const GemmProblem& g, int want_stages, cudaStream_t
     return check_launch("tc_gemm_pair_kernel");
 }
 
+// Lean library (the paper's deployment build, KP_LEAN): only the kernel
+// instantiations the compiled selectors can return exist; the generated
+// generated/tc_lean.h lists them as (es, bn, a_mn, b_mn, kind) with kind
+// 1 = one tile per CTA, 2 = persistent, 3 = CTA pair.
+#ifdef KP_LEAN
+#include "generated/tc_lean.h"
+#else
+constexpr bool lean_allowed(int, int, bool, bool, int) { return true; }
+#endif
+
+template <int ES, int BN, bool A_MN, bool B_MN>
+static kp_status pair_checked(const GemmProblem& g, int stages, cudaStream_t s) {
+    if constexpr (lean_allowed(ES, BN, A_MN, B_MN, 3))
+        return launch_pair<ES, BN, A_MN, B_MN>(g, stages, s);
+    else
+        return fail(KP_ERR_UNSUPPORTED, "kernel not in the lean library");
+}
+
+template <int ES, int BN, bool A_MN, bool B_MN, int NBUF>
+static kp_status tile_checked(const GemmProblem& g, int stages, cudaStream_t s) {
+    if constexpr (lean_allowed(ES, BN, A_MN, B_MN, NBUF))
+        return launch_t<ES, BN, A_MN, B_MN, NBUF>(g, stages, s);
+    else
+        return fail(KP_ERR_UNSUPPORTED, "kernel not in the lean library");
+}
+
 template <int ES, int BN>
 static kp_status by_layout_pair(const GemmProblem& g, int stages, cudaStream_t s) {
-    if (!g.ta && g.tb) return launch_pair<ES, BN, false, false>(g, stages, s);
-    if (!g.ta && !g.tb) return launch_pair<ES, BN, false, true>(g, stages, s);
-    if (g.ta && g.tb) return launch_pair<ES, BN, true, false>(g, stages, s);
-    return launch_pair<ES, BN, true, true>(g, stages, s);
+    if (!g.ta && g.tb) return pair_checked<ES, BN, false, false>(g, stages, s);
+    if (!g.ta && !g.tb) return pair_checked<ES, BN, false, true>(g, stages, s);
+    if (g.ta && g.tb) return pair_checked<ES, BN, true, false>(g, stages, s);
+    return pair_checked<ES, BN, true, true>(g, stages, s);
 }
 
 template <int ES>
@@ -982,10 +1023,10 @@ static kp_status by_tile_pair(const kp_config& c, const GemmProblem& g, cudaStre
 template <int ES, int BN, int NBUF>
 static kp_status by_layout(const GemmProblem& g, int stages, cudaStream_t s) {
     // A normal = K-major, A transposed = MN-major; B transposed = K-major, B normal = MN-major
-    if (!g.ta && g.tb) return launch_t<ES, BN, false, false, NBUF>(g, stages, s);
-    if (!g.ta && !g.tb) return launch_t<ES, BN, false, true, NBUF>(g, stages, s);
-    if (g.ta && g.tb) return launch_t<ES, BN, true, false, NBUF>(g, stages, s);
-    return launch_t<ES, BN, true, true, NBUF>(g, stages, s);
+    if (!g.ta && g.tb) return tile_checked<ES, BN, false, false, NBUF>(g, stages, s);
+    if (!g.ta && !g.tb) return tile_checked<ES, BN, false, true, NBUF>(g, stages, s);
+    if (g.ta && g.tb) return tile_checked<ES, BN, true, false, NBUF>(g, stages, s);
+    return tile_checked<ES, BN, true, true, NBUF>(g, stages, s);
 }
 
 template <int ES, int NBUF>

@@ -372,3 +372,30 @@ def set_skinny(mode: int) -> int:
 
 def launch_count() -> int:
     return int(nat.lib().kp_launch_count())
+
+
+_OP = None
+
+
+def torch_op():
+    """Register (once) and return ``torch.ops.kernelprune.matmul(a, b, family)``:
+    the runtime-selected GEMM (kp_gemm_auto) as a PyTorch custom operator, so
+    the deployed library is callable from torch code, torch.compile graphs and
+    TorchScript-free C++ callers of the dispatcher alike. A fake (meta)
+    implementation gives shape/dtype propagation without a launch."""
+    global _OP
+    if _OP is not None:
+        return _OP
+    torch = _torch()
+
+    @torch.library.custom_op("kernelprune::matmul", mutates_args=(),
+                             schema="(Tensor a, Tensor b, str family) -> Tensor")
+    def _matmul(a, b, family):
+        return matmul(a, b, None, family=family)
+
+    @_matmul.register_fake
+    def _(a, b, family):
+        return a.new_empty(a.shape[:-1] + b.shape[-1:], dtype=torch.float32)
+
+    _OP = torch.ops.kernelprune.matmul
+    return _OP

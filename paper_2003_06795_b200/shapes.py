@@ -96,6 +96,13 @@ PROBLEM_SETS = {
     "networks+squares": lambda: tuple(dict.fromkeys(
         network_problems(batches=(1, 2, 4, 8, 16))
         + square_problems((64, 128, 256, 512, 1024, 2048, 4096, 8192)))),
+    # round-2 tensor-core training set: the network shapes plus squares up
+    # to 8192 including 3072 / 6144, so the trees see the large-size regime
+    # between the bench squares and 8192 (round-1 selectors picked small
+    # tiles at held-out 4096^3)
+    "networks+squares-large": lambda: tuple(dict.fromkeys(
+        network_problems(batches=(1, 2, 4, 8, 16))
+        + square_problems((64, 128, 256, 512, 1024, 2048, 3072, 4096, 6144, 8192)))),
     # the row added to the round-1 datasets after their first sweep
     "square-8192": lambda: square_problems((8192,)),
     # generalisation check: the batch-32/64 network shapes the selectors were

@@ -350,3 +350,18 @@ def test_runtime_selection_every_layout(ta, tb):
         want = gemm_f32_exact(a_store, b_store, m=m, k=k, n=n, trans_a=ta,
                               trans_b=tb).reshape(m, n)
         np.testing.assert_array_equal(got, want, err_msg=f"{(m, k, n)} {cfg}")
+
+
+def test_registered_torch_op():
+    """torch.ops.kernelprune.matmul is the runtime-selected library call."""
+    gemm = _gemm()
+    op = gemm.torch_op()
+    a = torch.rand(300, 200, device="cuda")
+    b = torch.rand(200, 100, device="cuda")
+    got = op(a, b, "f32")
+    assert torch.equal(got, gemm.matmul(a, b))
+    # the fake implementation propagates shapes without launching
+    from torch._subclasses.fake_tensor import FakeTensorMode
+    with FakeTensorMode():
+        fa, fb = torch.empty(7, 5, device="cuda"), torch.empty(5, 3, device="cuda")
+        assert op(fa, fb, "f32").shape == (7, 3)

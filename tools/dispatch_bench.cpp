@@ -31,19 +31,21 @@ int main() {
     const char* fams[] = {"f32", "tf32", "bf16"};
     bool first = true;
     for (int f = 0; f < 3; ++f)
-        for (int tb = 0; tb < 2; ++tb) {
+        for (int lay = 0; lay < 4; ++lay) {
+            const int ta = lay >> 1, tb = lay & 1;
             kp_config c;
-            if (kp_select(kp_family(f), 0, tb, 64, 64, 64, &c) != KP_OK) continue;
+            if (kp_select(kp_family(f), ta, tb, 64, 64, 64, &c) != KP_OK) continue;
             const int iters = 4'000'000;
             uint32_t sink = 0;
             auto t0 = clk::now();
             for (int i = 0; i < iters; ++i) {
                 const int64_t* s = &shapes[3 * (i & 4095)];
-                kp_select(kp_family(f), 0, tb, s[0], s[1], s[2], &c);
+                kp_select(kp_family(f), ta, tb, s[0], s[1], s[2], &c);
                 sink += c.acc;
             }
             double ns = std::chrono::duration<double, std::nano>(clk::now() - t0).count() / iters;
-            std::printf("%s\"%s_%s\": %.1f", first ? "" : ", ", fams[f], tb ? "nt" : "nn", ns);
+            static const char* lays[] = {"nn", "nt", "tn", "tt"};
+            std::printf("%s\"%s_%s\": %.1f", first ? "" : ", ", fams[f], lays[lay], ns);
             first = false;
             if (sink == 0xFFFFFFFF) std::printf(" ");
         }
