@@ -329,7 +329,7 @@ kp_status kp_sweep_problem_ex(kp_family family, const kp_config* cfgs, int32_t n
     GemmProblem g;
     if ((st = to_problem(desc, A, B, C, &g)) != KP_OK) return st;
     for (int32_t i = 0; i < n_cfgs; ++i)
-        if ((st = valid_config(family, cfgs[i])) != KP_OK) return st;
+        if (!is_skinny(cfgs[i]) && (st = valid_config(family, cfgs[i])) != KP_OK) return st;
     // With KP_SWEEP_EARLY_EXIT, a config whose first launch is both over 1 ms
     // and 8x the best median of this call so far keeps that single timing: it
     // normalises below 0.125 either way and the extra launches would dominate

@@ -557,7 +557,6 @@ tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap map_a,
     }
     fence_before_sync();
     cluster_sync();  // both CTAs' barriers exist before any remote arrive / multicast
-    __syncthreads();  // (CTA-scope ordering of the TMEM slot write for the race checker)
     fence_after_sync();
     const uint32_t tmem = *tmem_slot;
 

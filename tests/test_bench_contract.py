@@ -17,8 +17,12 @@ KEYS = ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
         "gpu_launches", "clocks", "roofline", "cpu_baseline")
 
 
+BENCH = ROOT / "profiles" / "bench_r02.json"
+BENCH_REF = ROOT / "profiles" / "bench_ref_r02.json"
+
+
 def test_committed_bench_line_has_contract_keys():
-    line = json.loads((ROOT / "profiles" / "bench_r01.json").read_text())
+    line = json.loads(BENCH.read_text())
     for k in KEYS:
         assert k in line, k
     assert line["warmup"] >= 3 and line["gpu_launches"] > 0
@@ -33,10 +37,48 @@ def test_committed_bench_line_has_contract_keys():
 
 
 def test_reference_arm_line():
-    line = json.loads((ROOT / "profiles" / "bench_ref_r01.json").read_text())
+    line = json.loads(BENCH_REF.read_text())
     assert line["impl"] == "reference"
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
     assert line["cpu_baseline"]["value"] == line["value"]
+    assert line["cpu_baseline"]["kind"] == "port"   # the oracle restatement
+
+
+def test_both_arms_share_config_and_metric():
+    ours, ref = json.loads(BENCH.read_text()), json.loads(BENCH_REF.read_text())
+    assert ours["config"] == ref["config"]
+    for k in ("metric", "unit", "higher_is_better", "steps", "warmup", "n_gpus"):
+        assert ours[k] == ref[k], k
+    import bench
+    assert bench.bench_config(1) == ours["config"]
+
+
+def test_roofline_blocks_follow_from_their_numbers():
+    import math
+    line = json.loads(BENCH.read_text())
+    roof = line["roofline"]
+    # FP32 headline against the nominal FMA-pipe peak, the >= 12 ms probe beside it
+    assert abs(roof["peak"] - line["peaks"]["fp32_nominal"]) < 1e-9
+    assert abs(roof["frac_of_measured"] - roof["achieved"] / roof["peak_measured"]) < 1e-9
+    cpu = line["cpu_baseline"]
+    assert cpu["kind"] == "port" and cpu["one_core"]["cores"] == 1 and cpu["cores"] >= 1
+    large = line["large_sizes"]
+    assert large["clocks"]["samples"] >= 1
+    assert not set(large["clocks"]["reasons"]) & {"hw_slowdown", "hw_thermal_slowdown",
+                                                  "sw_thermal_slowdown"}
+    for row in large["rows"]:
+        peak = large["summary"][row["family"]]["peak"]
+        assert abs(row["selected_frac"] - row["selected_tflops"] / peak) < 1e-9
+        assert row["best_tflops"] >= row["selected_tflops"]
+    for fam, blk in line["network_roofline"].items():
+        fr = [r["frac"] for r in blk["rows"]]
+        assert abs(blk["geomean_frac"] - math.exp(sum(map(math.log, fr)) / len(fr))) < 1e-9
+        assert all(r["mkn"][0] * r["mkn"][1] * r["mkn"][2] * 2 >= 1e9 for r in blk["rows"])
+    for fam, blk in line["held_out"].items():
+        for part in ("held_out_split", "unseen_batch32_64"):
+            assert 0 < blk[part]["pct_oracle_best"] <= 100.0
+    for fam, blk in line["small_m"].items():
+        assert all(r["mkn"][0] <= 16 for r in blk["rows"])
 
 
 def test_clock_sampler_keeps_samples_inside_the_region(tmp_path):
