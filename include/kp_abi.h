@@ -186,9 +186,16 @@ int32_t   kp_set_skinny(int32_t mode);
  * selector is compiled in for this family / transpose variant. */
 kp_status kp_select(kp_family family, int32_t trans_a, int32_t trans_b,
                     int64_t m, int64_t k, int64_t n, kp_config* out);
+/* kp_select for a strided-batched problem: batch 1 uses the plain selector;
+ * batch > 1 the selector trained on the strided-batched dataset whose batch
+ * count is closest (log scale) -- one selector per (family, trans, batch)
+ * variant, SURVEY H5 -- else the plain one.  kp_gemm_auto calls this with
+ * desc->batch. */
+kp_status kp_select_ex(kp_family family, int32_t trans_a, int32_t trans_b, int64_t batch,
+                       int64_t m, int64_t k, int64_t n, kp_config* out);
 /* What kp_gemm_auto launches for this shape: kp_select's config, or the
  * all-zero config when the small-M path takes the problem. */
-kp_status kp_auto_config(kp_family family, int32_t trans_a, int32_t trans_b,
+kp_status kp_auto_config(kp_family family, int32_t trans_a, int32_t trans_b, int64_t batch,
                          int64_t m, int64_t k, int64_t n, kp_config* out);
 kp_status kp_gemm_auto(kp_family family, const kp_gemm_desc* desc,
                        const void* A, const void* B, float* C, void* stream,

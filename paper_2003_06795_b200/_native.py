@@ -34,7 +34,7 @@ EXPORTS = ("kp_abi_version", "kp_num_configs", "kp_config_at", "kp_config_valid"
            "kp_fp32_peak", "kp_conv_output_shape", "kp_im2col", "kp_conv2d_auto",
            "kp_set_schedule", "kp_sweep_problem_ex", "kp_set_tc_split",
            "kp_gemm_skinny", "kp_set_skinny", "kp_auto_config", "kp_im2col_pitched",
-           "kp_conv_workspace_elems")
+           "kp_conv_workspace_elems", "kp_select_ex")
 
 
 class KpConfig(ctypes.Structure):
@@ -113,7 +113,9 @@ def _declare(lib):
         "kp_set_tc_split": (c.c_int32, [c.c_int32]),
         "kp_set_skinny": (c.c_int32, [c.c_int32]),
         "kp_auto_config": (c.c_int, [c.c_int, c.c_int32, c.c_int32, c.c_int64, c.c_int64,
-                                     c.c_int64, P(KpConfig)]),
+                                     c.c_int64, c.c_int64, P(KpConfig)]),
+        "kp_select_ex": (c.c_int, [c.c_int, c.c_int32, c.c_int32, c.c_int64, c.c_int64,
+                                   c.c_int64, c.c_int64, P(KpConfig)]),
         "kp_gemm_skinny": (c.c_int, [c.c_int, P(KpGemmDesc), c.c_void_p, c.c_void_p,
                                      c.c_void_p, c.c_void_p]),
         "kp_conv_output_shape": (c.c_int, [P(KpConvDesc), P(c.c_int64), P(c.c_int64)]),

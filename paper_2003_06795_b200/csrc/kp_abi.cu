@@ -361,28 +361,46 @@ kp_status kp_sweep_problem(kp_family family, const kp_config* cfgs, int32_t n_cf
                                max_cell_ns, KP_SWEEP_EARLY_EXIT, runtime_ns, stream);
 }
 
-kp_status kp_select(kp_family family, int32_t trans_a, int32_t trans_b, int64_t m, int64_t k,
-                    int64_t n, kp_config* out) {
+kp_status kp_select_ex(kp_family family, int32_t trans_a, int32_t trans_b, int64_t batch,
+                       int64_t m, int64_t k, int64_t n, kp_config* out) {
     if (!out) return fail(KP_ERR_INVALID_ARG, "null output");
-    if (m < 1 || k < 1 || n < 1) return fail(KP_ERR_BAD_SHAPE, "problem dims must be >= 1");
+    if (m < 1 || k < 1 || n < 1 || batch < 1) return fail(KP_ERR_BAD_SHAPE, "problem dims must be >= 1");
+    // batch 1: the plain selector; batch > 1: the strided-batched selector
+    // whose dataset batch is closest in log scale, else the plain one
+    const KpSelectorEntry* best = nullptr;
+    double best_d = 0.0;
     for (int i = 0; i < kp_num_selectors; ++i) {
         const KpSelectorEntry& e = kp_selectors[i];
-        if (e.fn && e.family == int(family) && e.trans_a == (trans_a != 0) &&
-            e.trans_b == (trans_b != 0)) {
-            *out = e.fn(m, k, n);
-            return KP_OK;
+        if (!e.fn || e.family != int(family) || e.trans_a != (trans_a != 0) ||
+            e.trans_b != (trans_b != 0))
+            continue;
+        if ((batch == 1) != (e.batch == 1)) {
+            if (batch == 1 || best) continue;  // plain problems never take a batched tree
+            best = &e;                          // batched problem: plain tree as fallback
+            best_d = 1e30;
+            continue;
         }
+        const double d = std::fabs(std::log(double(e.batch)) - std::log(double(batch)));
+        if (!best || d < best_d) { best = &e; best_d = d; }
     }
-    return fail(KP_ERR_UNSUPPORTED, "no selector compiled in for this family / transpose variant");
+    if (!best)
+        return fail(KP_ERR_UNSUPPORTED, "no selector compiled in for this family / transpose variant");
+    *out = best->fn(m, k, n);
+    return KP_OK;
 }
 
-kp_status kp_auto_config(kp_family family, int32_t trans_a, int32_t trans_b, int64_t m, int64_t k,
-                         int64_t n, kp_config* out) {
+kp_status kp_select(kp_family family, int32_t trans_a, int32_t trans_b, int64_t m, int64_t k,
+                    int64_t n, kp_config* out) {
+    return kp_select_ex(family, trans_a, trans_b, 1, m, k, n, out);
+}
+
+kp_status kp_auto_config(kp_family family, int32_t trans_a, int32_t trans_b, int64_t batch,
+                         int64_t m, int64_t k, int64_t n, kp_config* out) {
     if (!out) return fail(KP_ERR_INVALID_ARG, "null output");
-    kp_status st = kp_select(family, trans_a, trans_b, m, k, n, out);
+    kp_status st = kp_select_ex(family, trans_a, trans_b, batch, m, k, n, out);
     if (st != KP_OK) return st;
     GemmProblem g{};
-    g.batch = 1; g.m = m; g.k = k; g.n = n;
+    g.batch = batch; g.m = m; g.k = k; g.n = n;
     if (skinny::eligible(family, g)) *out = kp_config{0, 0, 0, 0, 0};
     return KP_OK;
 }
@@ -391,7 +409,8 @@ kp_status kp_gemm_auto(kp_family family, const kp_gemm_desc* desc, const void* A
                        float* C, void* stream, kp_config* chosen) {
     if (!desc) return fail(KP_ERR_INVALID_ARG, "null gemm descriptor");
     kp_config cfg;
-    kp_status st = kp_select(family, desc->trans_a, desc->trans_b, desc->m, desc->k, desc->n, &cfg);
+    kp_status st = kp_select_ex(family, desc->trans_a, desc->trans_b, desc->batch, desc->m, desc->k,
+                                desc->n, &cfg);
     if (st != KP_OK) return st;
     GemmProblem g;
     if ((st = to_problem(desc, A, B, C, &g)) != KP_OK) return st;

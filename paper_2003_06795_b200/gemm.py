@@ -344,20 +344,23 @@ def family_configs(family="f32") -> tuple[KernelConfig, ...]:
     return tuple(out)
 
 
-def select(m: int, k: int, n: int, *, family="f32", trans_a=False, trans_b=False) -> KernelConfig:
-    """The config the compiled runtime selector returns for (m, k, n)."""
+def select(m: int, k: int, n: int, *, family="f32", trans_a=False, trans_b=False,
+           batch: int = 1) -> KernelConfig:
+    """The config the compiled runtime selector returns for (m, k, n) (the
+    strided-batched selector when batch > 1, kp_select_ex)."""
     cfg = nat.KpConfig()
-    nat.check(nat.lib().kp_select(nat.family_id(family), int(trans_a), int(trans_b), m, k, n,
-                                  ctypes.byref(cfg)), "kp_select")
+    nat.check(nat.lib().kp_select_ex(nat.family_id(family), int(trans_a), int(trans_b), batch,
+                                     m, k, n, ctypes.byref(cfg)), "kp_select_ex")
     return KernelConfig(*cfg.as_tuple())
 
 
-def auto_config(m: int, k: int, n: int, *, family="f32", trans_a=False, trans_b=False):
+def auto_config(m: int, k: int, n: int, *, family="f32", trans_a=False, trans_b=False,
+                batch: int = 1):
     """What kp_gemm_auto runs for (m, k, n): the selector's KernelConfig, or
     "skinny" when the small-M path (m <= 16) takes the problem."""
     cfg = nat.KpConfig()
-    nat.check(nat.lib().kp_auto_config(nat.family_id(family), int(trans_a), int(trans_b), m, k,
-                                       n, ctypes.byref(cfg)), "kp_auto_config")
+    nat.check(nat.lib().kp_auto_config(nat.family_id(family), int(trans_a), int(trans_b), batch,
+                                       m, k, n, ctypes.byref(cfg)), "kp_auto_config")
     t = cfg.as_tuple()
     return nat.SKINNY if t == (0, 0, 0, 0, 0) else KernelConfig(*t)
 

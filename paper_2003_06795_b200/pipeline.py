@@ -130,14 +130,17 @@ def main(argv=None) -> int:
     ap.add_argument("--method", default="auto", choices=pruning.METHODS + ("auto",),
                     help="pruning method; auto = 5-fold CV on the training split")
     ap.add_argument("--budget", type=int, default=8)
+    ap.add_argument("--batch", type=int, default=1,
+                    help="batch count of a strided-batched dataset (selector variant _b<N>)")
     ap.add_argument("--seed", type=int, default=42)
     ap.add_argument("--survey", action="store_true", help="also score every method x budget")
     ap.add_argument("--no-build", action="store_true")
     args = ap.parse_args(argv)
-    summary = build_selector(args.data, args.family, args.trans, args.method, args.budget,
+    variant = args.trans if args.batch == 1 else f"{args.trans}_b{args.batch}"
+    summary = build_selector(args.data, args.family, variant, args.method, args.budget,
                              args.seed)
     print(json.dumps(summary, indent=2))
-    out_dir = SEL_DIR / f"{args.family}_{args.trans}"
+    out_dir = SEL_DIR / f"{args.family}_{variant}"
     if args.survey:
         split = dataset.split(load_matrix(args.data), 0.2, args.seed)
         rows = choose(split, ("top-count", "kmeans", "pca-kmeans", "decision-tree"),
@@ -146,7 +149,7 @@ def main(argv=None) -> int:
         for r in rows:
             print(f"{r['method']:14s} {r['budget']:2d} ceiling {r['ceiling']:6.2f} "
                   f"dt {r['decision_tree']:6.2f}")
-    libgen.install_model(out_dir / "model.json", args.family, args.trans)
+    libgen.install_model(out_dir / "model.json", args.family, variant)
     libgen.write_selector_table()
     if not args.no_build:
         from .build import build_library

@@ -103,6 +103,14 @@ PROBLEM_SETS = {
     "networks+squares-large": lambda: tuple(dict.fromkeys(
         network_problems(batches=(1, 2, 4, 8, 16))
         + square_problems((64, 128, 256, 512, 1024, 2048, 3072, 4096, 6144, 8192)))),
+    # strided-batched variant (batch dimension explicit instead of folded into
+    # M): the per-image conv GEMMs of the three networks (FC layers
+    # are one GEMM over the batch, not a batched one) plus squares up to 1024;
+    # swept with --batch 8
+    "networks-per-image": lambda: tuple(dict.fromkeys(
+        tuple(ProblemSize(hw, k, n) for net in NETWORKS.values() for _, hw, k, n in net
+              if hw > 1)
+        + square_problems((64, 128, 256, 512, 1024)))),
     # the row added to the round-1 datasets after their first sweep
     "square-8192": lambda: square_problems((8192,)),
     # generalisation check: the batch-32/64 network shapes the selectors were

@@ -124,3 +124,28 @@ def test_lean_library_only_has_selected_kernels():
     assert rc == nat.KP_ERR_UNSUPPORTED
     assert b"lean" in lib.kp_last_error()
     assert LEAN.stat().st_size < nat.LIB_PATH.stat().st_size
+
+
+def test_batched_selector_dispatch():
+    """kp_select_ex: batch 1 answers from the plain tree; batch > 1 from the
+    strided-batched tree of the same (family, layout) when one is compiled in
+    (selector variant <layout>_b<N>), else from the plain tree."""
+    from paper_2003_06795_b200 import codegen, libgen, selector_models
+    root = Path(__file__).resolve().parents[1]
+    lib = nat.lib()
+    cfg = nat.KpConfig()
+    batched = {(f, t[:2]): libgen.variant_batch(t) for f, t in libgen.installed() if "_b" in t}
+    for fam, fid in nat.FAMILIES.items():
+        plain = codegen.export_tree(selector_models.load_model(
+            root / "selectors" / f"{fam}_nn" / "model.json"))
+        for (m, k, n) in [(784, 576, 64), (3136, 1152, 128), (49, 4608, 512)]:
+            assert lib.kp_select_ex(fid, 0, 0, 1, m, k, n, ctypes.byref(cfg)) == nat.KP_OK
+            assert cfg.as_tuple() == codegen.traverse_document(plain, m, k, n).as_tuple()
+            assert lib.kp_select_ex(fid, 0, 0, 8, m, k, n, ctypes.byref(cfg)) == nat.KP_OK
+            if (fam, "nn") in batched:
+                bt = codegen.export_tree(selector_models.load_model(
+                    root / "selectors" / f"{fam}_nn_b{batched[(fam, 'nn')]}" / "model.json"))
+                assert cfg.as_tuple() == codegen.traverse_document(bt, m, k, n).as_tuple()
+            else:
+                assert cfg.as_tuple() == codegen.traverse_document(plain, m, k, n).as_tuple()
+    assert lib.kp_select_ex(0, 0, 0, 0, 8, 8, 8, ctypes.byref(cfg)) == nat.KP_ERR_BAD_SHAPE

@@ -365,3 +365,28 @@ def test_registered_torch_op():
     with FakeTensorMode():
         fa, fb = torch.empty(7, 5, device="cuda"), torch.empty(5, 3, device="cuda")
         assert op(fa, fb, "f32").shape == (7, 3)
+
+
+def test_batched_runtime_selection():
+    """Strided-batched problems dispatch through the batched selector
+    (select_f32_nn_b8, kp_select_ex with batch > 1) and stay bit-exact."""
+    import ctypes
+    from paper_2003_06795_b200 import _native as nat
+    gemm = _gemm()
+    for (bt, m, k, n) in [(8, 784, 576, 64), (3, 196, 2304, 256), (8, 49, 512, 2048)]:
+        rng = np.random.default_rng(bt * m + k)
+        a = rng.uniform(-1, 1, (bt, m, k)).astype(np.float32)
+        b = rng.uniform(-1, 1, (bt, k, n)).astype(np.float32)
+        cfg = gemm.select(m, k, n, batch=bt)
+        assert gemm.auto_config(m, k, n, batch=bt) == cfg
+        got = gemm.matmul(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()).cpu().numpy()
+        want = gemm_f32_exact(a, b, m=m, k=k, n=n, batch=bt, stride_a=m * k, stride_b=k * n,
+                              stride_c=m * n).reshape(bt, m, n)
+        np.testing.assert_array_equal(got, want, err_msg=f"{(bt, m, k, n)} {cfg}")
+        # kp_gemm_auto reports the batched tree's pick
+        d, da, db, dc = gemm.describe(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda())
+        chosen = nat.KpConfig()
+        nat.check(nat.lib().kp_gemm_auto(nat.F32_SIMT, ctypes.byref(d), da.data_ptr(),
+                                         db.data_ptr(), dc.data_ptr(), None, ctypes.byref(chosen)))
+        torch.cuda.synchronize()
+        assert chosen.as_tuple() == cfg.as_tuple()

@@ -54,7 +54,7 @@ def test_compiled_selector_matches_committed_model():
         assert header == codegen.emit_selector_source(doc, libgen.symbol_for(family, trans))
         for p in codegen.parity_grid()[::97]:
             got = gemm.select(p.m, p.k, p.n, family=family, trans_a=trans[0] == "t",
-                              trans_b=trans[1] == "t")
+                              trans_b=trans[1] == "t", batch=libgen.variant_batch(trans))
             assert got == codegen.traverse_document(doc, p.m, p.k, p.n), p
 
 
