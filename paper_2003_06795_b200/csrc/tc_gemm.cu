@@ -57,7 +57,12 @@ constexpr int BM = 128;
 constexpr int NUM_THREADS = 192;
 constexpr int GROUP_M = 8;  // default raster group (tc_group_m())
 constexpr int STAGE_ALIGN = 1024;
-constexpr int EPI_PITCH = 33;  // padded 32x32 staging tile per epilogue warp
+constexpr int EPI_PITCH = 33;  // padded 32x32 staging tile per epilogue warp (fallback path)
+// Epilogue shared memory: per epilogue warp two 32x32 fp32 buffers (4 KB,
+// 128B-swizzled rows) for the TMA-store path; the fallback path's padded
+// staging tiles fit in the same 32 KB.
+constexpr int EPI_BUF = 32 * 32 * 4;
+constexpr int EPI_BYTES = 4 * 2 * EPI_BUF;
 
 struct TcParams {
     float* C;
@@ -70,6 +75,7 @@ struct TcParams {
     int a_batch, b_batch;  // 1 if the operand advances with the batch index, else 0
     int splits;            // K splits per tile (1 = no split-K)
     int group_m;           // m-tiles per raster group
+    int tma_store;         // 1: C tile stored by TMA (beta == 0, aligned C, no split-K)
     float* ws;             // split-K partial tiles [tile][split][BM][BN] (splits > 1)
 };
 
@@ -129,6 +135,27 @@ __device__ __forceinline__ void fence_after_sync() {
 __device__ __forceinline__ void fence_before_sync() {
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
+
+// KP_TC_DEBUG builds (libkp_debug.so) record per-CTA phase timestamps
+// (%globaltimer, ns) of the 1-CTA kernel for the first TRACE_CTAS CTAs of a
+// launch: 0 entry, 1 setup done, 2 first TMA issued, 3 first stage landed,
+// 4 last MMA issued, 5 accumulator complete (epilogue), 6 stores issued,
+// 7 exit; 8.. epilogue warp 2, TMA-store path: chunk c's TMEM data in
+// registers (8 + 2c) and its store issued (9 + 2c), first 4 chunks.
+// kp_tc_trace_dump() copies them out (tools/tc_trace.py).
+#ifdef KP_TC_DEBUG
+constexpr int TRACE_CTAS = 4096;
+__device__ unsigned long long g_tc_trace[TRACE_CTAS][16];
+__device__ __forceinline__ void trace(int slot) {
+    if (blockIdx.x < TRACE_CTAS) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_tc_trace[blockIdx.x][slot] = t;
+    }
+}
+#else
+__device__ __forceinline__ void trace(int) {}
+#endif
 
 // UMMA shared-memory descriptor (Blackwell version bits = 1). layout: 2 =
 // SWIZZLE_128B, 4 = SWIZZLE_64B, 1 = SWIZZLE_128B_BASE32B.
@@ -203,6 +230,91 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// ------------------------------------------------------- TMA-store epilogue
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, uint32_t src, int c0, int c1,
+                                             int c2) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];"
+                 :: "l"(reinterpret_cast<uint64_t>(map)), "r"(src), "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" :: "n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// One epilogue warp stores its 32 rows x `cols` of the accumulator through
+// TMA: per 32-column chunk, tcgen05.ld (lane = row), alpha, 8 STS.128 into a
+// 128B-swizzled 32x32 buffer (chunk j of row r at r*128 + ((j ^ (r & 7)) << 4):
+// the 8 lanes of a quarter-warp hit 8 distinct bank groups), then lane 0
+// issues one bulk tensor store -- TMA clips rows / columns past the tensor,
+// so no bounds checks -- double-buffered against the store still reading the
+// other buffer.  `it` counts this warp's chunks across tiles.
+__device__ __forceinline__ void tmem_ld32_async(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+        "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+          "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+          "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+          "=r"(r[31])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() {
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void epi_tma_tile(const CUtensorMap* map_c, uint32_t taddr, int cols,
+                                             int n0, int row0, int bz, float alpha,
+                                             uint32_t bufs, int lane, int& it,
+                                             bool trace_warp = false) {
+    // the next chunk's TMEM load is in flight while this one is staged
+    uint32_t nxt[32];
+    tmem_ld32_async(taddr, nxt);
+#pragma unroll 1
+    for (int c0 = 0; c0 < cols; c0 += 32, ++it) {
+        tmem_wait_ld();
+        // the registers are defined only after the wait: re-bind them here so
+        // the compiler cannot read them before it
+#pragma unroll
+        for (int j = 0; j < 32; ++j) asm volatile("" : "+r"(nxt[j]));
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(nxt[j]);
+        if (trace_warp && lane == 0 && c0 < 128) trace(8 + 2 * (c0 >> 5));
+        if (c0 + 32 < cols) tmem_ld32_async(taddr + c0 + 32, nxt);
+        const uint32_t buf = bufs + uint32_t(it & 1) * EPI_BUF;
+        if (it >= 2) {  // the store issued from this buffer two chunks ago has read it
+            if (lane == 0) bulk_wait_read<1>();
+            __syncwarp();
+        }
+        const uint32_t row = buf + uint32_t(lane) * 128u;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const uint32_t addr = row + (uint32_t(j ^ (lane & 7)) << 4);
+            asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};"
+                         :: "r"(addr), "f"(alpha * v[4 * j]), "f"(alpha * v[4 * j + 1]),
+                            "f"(alpha * v[4 * j + 2]), "f"(alpha * v[4 * j + 3]) : "memory");
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+            tma_store_3d(map_c, buf, n0 + c0, row0, bz);
+            bulk_commit();
+            if (trace_warp && c0 < 128) trace(9 + 2 * (c0 >> 5));
+        }
+    }
+    tmem_wait_ld();  // (no load is outstanding here; keeps the fence before acc_empty honest)
+}
+
 // ------------------------------------------------------------------ kernel
 // Tile t (0 <= t < tiles_m*tiles_n*batch): batch-major, then a grouped raster
 // of GROUP_M m-tiles sweeping n inside each batch.
@@ -227,7 +339,7 @@ __device__ __forceinline__ void tile_coords(int t, const TcParams& p, int bn, in
 template <int ES, int BN, bool A_MN, bool B_MN, int NBUF>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-               const TcParams p) {
+               const __grid_constant__ CUtensorMap map_c, const TcParams p) {
     constexpr int ROW = 128;                  // bytes of K per operand row per stage
     constexpr int BK = ROW / ES;              // K elements per stage
     constexpr int UMMA_K = 32 / ES;           // K per tcgen05.mma
@@ -240,15 +352,17 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     constexpr uint32_t TMEM_COLS = BN * NBUF;
 
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    // 1024-byte aligned stage ring, then barriers, TMEM slot, epilogue staging
+    // 1024-byte aligned stage ring, epilogue buffers (1024-aligned), barriers, TMEM slot
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + STAGE_ALIGN - 1) & ~uint32_t(STAGE_ALIGN - 1);
     uint8_t* gbase = smem_raw + (base - raw);
     const int S = p.stages;
+    const uint32_t epi = base + S * STAGE_BYTES;
+    float* staging = reinterpret_cast<float*>(gbase + S * STAGE_BYTES);
     // barriers: full[S], empty[S], acc_full[2], acc_empty[2]
-    const uint32_t bars = base + S * STAGE_BYTES;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + S * STAGE_BYTES + (2 * S + 4) * 8);
-    float* staging = reinterpret_cast<float*>(gbase + S * STAGE_BYTES + (2 * S + 5) * 8);
+    const uint32_t bars = epi + EPI_BYTES;
+    uint32_t* tmem_slot =
+        reinterpret_cast<uint32_t*>(gbase + S * STAGE_BYTES + EPI_BYTES + (2 * S + 4) * 8);
     auto full_bar = [&](int s) { return bars + 8u * s; };
     auto empty_bar = [&](int s) { return bars + 8u * (S + s); };
     auto acc_full = [&](int b) { return bars + 8u * (2 * S + b); };
@@ -256,6 +370,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) trace(0);
     const int units = p.tiles_m * p.tiles_n * p.batch * p.splits;  // (tile, K split) work units
     // let the split-K reduce kernel's launch start now; its griddepcontrol.wait
     // still waits for this whole grid to finish and flush
@@ -273,6 +388,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
         asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
+        if (p.tma_store)
+            asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(&map_c)) : "memory");
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
@@ -283,6 +400,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     __syncthreads();
     fence_after_sync();
     const uint32_t tmem = *tmem_slot;
+    if (threadIdx.x == 0) trace(1);
 
     if (warp == 0) {
         if (lane == 0) {  // ---- TMA producer: one ring across all of this CTA's units
@@ -316,6 +434,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                             tma_load_3d(sb + j * BK * MB::W, &map_b, n0 + j * MB::ATOM, k0, zb,
                                         full_bar(s));
                     }
+                    if (kt_all == 0) trace(2);
                 }
             }
         }
@@ -335,6 +454,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                     const uint32_t phase = (kt_all / S) & 1;
                     mbar_wait(full_bar(s), phase);
                     fence_after_sync();
+                    if (kt_all == 0) trace(3);
                     const uint32_t sa = base + s * STAGE_BYTES;
                     const uint32_t sb = sa + A_BYTES;
 #pragma unroll
@@ -353,12 +473,14 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                     umma_commit(empty_bar(s));  // frees the stage once these MMAs retire
                 }
                 umma_commit(acc_full(buf));     // accumulator of this tile complete
+                trace(4);
             }
         }
     } else {  // ---- epilogue warps 2..5: TMEM lane quarter = warp % 4
         const int q = warp & 3;
         float* st = staging + (warp - 2) * 32 * EPI_PITCH;
-        int it = 0;
+        const uint32_t ebufs = epi + uint32_t(warp - 2) * 2 * EPI_BUF;
+        int it = 0, eit = 0;
         for (int u = blockIdx.x; u < units; u += gridDim.x, ++it) {
             const int t = u / p.splits;
             int m0, n0, bz;
@@ -367,10 +489,21 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             const uint32_t use = NBUF == 2 ? ((it >> 1) & 1) : (it & 1);
             mbar_wait(acc_full(buf), use);
             fence_after_sync();
+            if (warp == 2 && lane == 0) trace(5);
             float* Cb = p.C + int64_t(bz) * p.sc;
             const int row0 = m0 + q * 32;
             const uint32_t taddr = tmem + (uint32_t(q * 32) << 16) + uint32_t(buf * BN);
             const int cols = min(BN, p.N - n0);
+            if (p.tma_store) {
+                epi_tma_tile(&map_c, taddr, cols, n0, row0, bz, p.alpha, ebufs, lane, eit,
+                             warp == 2 && it == 0);
+                if (warp == 2 && lane == 0) trace(6);
+                fence_before_sync();  // the tcgen05.ld of this tile are complete
+                if (lane == 0)
+                    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(acc_empty(buf))
+                                 : "memory");
+                continue;
+            }
             // split-K: this unit's partial tile, full BM x BN, row-major
             float* part = p.splits > 1
                 ? p.ws + (int64_t(t) * p.splits + u % p.splits) * (BM * BN) : nullptr;
@@ -401,6 +534,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
                 }
                 __syncwarp();
             }
+            if (warp == 2 && lane == 0) trace(6);
             fence_before_sync();
             if (lane == 0) {
                 asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(acc_empty(buf))
@@ -408,6 +542,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             }
         }
     }
+    if (p.tma_store && warp >= 2 && lane == 0) bulk_wait_all();  // stores out of smem
     fence_before_sync();
     __syncthreads();
     if (warp == 1) {
@@ -415,6 +550,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem),
                      "r"(TMEM_COLS) : "memory");
     }
+    if (threadIdx.x == 0) trace(7);
 }
 
 // Split-K reduction: one thread per 4 consecutive columns of one tile row;
@@ -500,7 +636,8 @@ constexpr uint32_t PEER_MASK = 0xFEFFFFFFu;  // shared::cluster address of the e
 template <int ES, int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap map_a,
-                    const __grid_constant__ CUtensorMap map_b, const TcParams p) {
+                    const __grid_constant__ CUtensorMap map_b,
+                    const __grid_constant__ CUtensorMap map_c, const TcParams p) {
     constexpr int ROW = 128;
     constexpr int BK = ROW / ES;
     constexpr int UMMA_K = 32 / ES;
@@ -520,9 +657,11 @@ tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap map_a,
     const uint32_t base = (raw + STAGE_ALIGN - 1) & ~uint32_t(STAGE_ALIGN - 1);
     uint8_t* gbase = smem_raw + (base - raw);
     const int S = p.stages;
-    const uint32_t bars = base + S * STAGE_BYTES;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + S * STAGE_BYTES + (2 * S + 4) * 8);
-    float* staging = reinterpret_cast<float*>(gbase + S * STAGE_BYTES + (2 * S + 5) * 8);
+    const uint32_t epi = base + S * STAGE_BYTES;
+    float* staging = reinterpret_cast<float*>(gbase + S * STAGE_BYTES);
+    const uint32_t bars = epi + EPI_BYTES;
+    uint32_t* tmem_slot =
+        reinterpret_cast<uint32_t*>(gbase + S * STAGE_BYTES + EPI_BYTES + (2 * S + 4) * 8);
     auto full_bar = [&](int s) { return bars + 8u * s; };
     auto empty_bar = [&](int s) { return bars + 8u * (S + s); };
     auto acc_full = [&](int b) { return bars + 8u * (2 * S + b); };
@@ -549,6 +688,8 @@ tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap map_a,
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
         asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
+        if (p.tma_store)
+            asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(&map_c)) : "memory");
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;"
@@ -631,7 +772,8 @@ tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap map_a,
     } else {  // ---- epilogue warps 2..5 of both CTAs: own 128 rows of D
         const int q = warp & 3;
         float* st = staging + (warp - 2) * 32 * EPI_PITCH;
-        int it = 0;
+        const uint32_t ebufs = epi + uint32_t(warp - 2) * 2 * EPI_BUF;
+        int it = 0, eit = 0;
         for (int t = pair; t < total; t += npairs, ++it) {
             int m0, n0, bz;
             tile_coords(t, p, BN, m0, n0, bz);
@@ -644,6 +786,14 @@ tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap map_a,
             const int row0 = m0 + q * 32;
             const uint32_t taddr = tmem + (uint32_t(q * 32) << 16) + uint32_t(buf * BN);
             const int cols = min(BN, p.N - n0);
+            if (p.tma_store) {
+                epi_tma_tile(&map_c, taddr, cols, n0, row0, bz, p.alpha, ebufs, lane, eit);
+                fence_before_sync();
+                if (lane == 0)
+                    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];"
+                                 :: "r"(acc_empty(buf) & PEER_MASK) : "memory");
+                continue;
+            }
 #pragma unroll 1
             for (int c0 = 0; c0 < cols; c0 += 32) {
                 float v[32];
@@ -672,6 +822,7 @@ tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap map_a,
             }
         }
     }
+    if (p.tma_store && warp >= 2 && lane == 0) bulk_wait_all();  // stores out of smem
     fence_before_sync();
     __syncthreads();
     cluster_sync();
@@ -702,9 +853,41 @@ static EncodeFn encoder() {
 }
 
 // 3-D tensor map over (inner, outer, batch) with a 128-byte swizzled box.
+// Encoded maps are cached per host thread (a small direct-mapped table keyed
+// by every encode argument): cuTensorMapEncodeTiled costs microseconds, and a
+// GEMM launch needs up to three of them -- on small problems the host enqueue,
+// not the kernel, would otherwise set the launch rate.  A map depends only on
+// its arguments (address, extents, strides, box, swizzle), so a hit is exact.
+struct MapKey {
+    const void* ptr;
+    int64_t inner, outer, batch, ld, bstride;
+    int box_inner, box_outer, swizzle, bf16;
+    bool operator==(const MapKey& o) const { return std::memcmp(this, &o, sizeof *this) == 0; }
+};
+struct MapSlot {
+    MapKey key;
+    CUtensorMap map;
+    bool valid;
+};
+
 static kp_status make_map(CUtensorMap* map, bool bf16, const void* ptr, int64_t inner,
                           int64_t outer, int64_t batch, int64_t ld, int64_t bstride, int box_inner,
                           int box_outer, int swizzle) {
+    MapKey key;
+    std::memset(&key, 0, sizeof key);  // padding bytes take part in the comparison
+    key.ptr = ptr; key.inner = inner; key.outer = outer; key.batch = batch; key.ld = ld;
+    key.bstride = batch > 1 ? bstride : 0; key.box_inner = box_inner; key.box_outer = box_outer;
+    key.swizzle = swizzle; key.bf16 = bf16;
+    constexpr int SLOTS = 64;
+    static thread_local MapSlot cache[SLOTS];
+    uint64_t h = reinterpret_cast<uintptr_t>(ptr) >> 4;
+    h = h * 0x9E3779B97F4A7C15ull ^ uint64_t(inner) * 31 ^ uint64_t(outer) * 131 ^
+        uint64_t(box_inner) * 7 ^ uint64_t(box_outer) * 13 ^ uint64_t(ld) * 17 ^ uint64_t(swizzle);
+    MapSlot& slot = cache[(h ^ (h >> 29)) % SLOTS];
+    if (slot.valid && slot.key == key) {
+        *map = slot.map;
+        return KP_OK;
+    }
     EncodeFn enc = encoder();
     if (!enc) return fail(KP_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
     const int es = bf16 ? 2 : 4;
@@ -717,6 +900,9 @@ static kp_status make_map(CUtensorMap* map, bool bf16, const void* ptr, int64_t 
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CUtensorMapSwizzle(swizzle),
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(KP_ERR_ALIGNMENT, "cuTensorMapEncodeTiled rejected the operand");
+    slot.key = key;
+    slot.map = *map;
+    slot.valid = true;
     return KP_OK;
 }
 
@@ -765,8 +951,7 @@ kp_status valid(kp_family fam, const kp_config& c) {
 }
 
 static size_t smem_bytes(int bn, int stages) {
-    return STAGE_ALIGN + size_t(stages) * (BM + bn) * 128 + (2 * stages + 6) * 8 +
-           4 * 32 * EPI_PITCH * 4;
+    return STAGE_ALIGN + size_t(stages) * (BM + bn) * 128 + EPI_BYTES + (2 * stages + 6) * 8;
 }
 
 static int sm_count() {
@@ -842,6 +1027,31 @@ static int choose_splits(int64_t tiles, int k_tiles, int bn) {
     return S < 2 ? 1 : int(S);
 }
 
+// TMA-store epilogue eligibility + C tensor map (fp32, 32x32 boxes, 128B
+// swizzle): beta == 0 (C write-only), 16-byte aligned C rows / batches, and
+// no split-K (partials take the workspace path).  KP_TC_TMA_STORE=0 turns it
+// off for A/B timing (tuning experiments only).
+static bool tma_store_on() {
+    static const bool on = [] {
+        const char* e = std::getenv("KP_TC_TMA_STORE");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+static kp_status c_map(const GemmProblem& g, int splits, CUtensorMap* mc, int* use) {
+    std::memset(mc, 0, sizeof *mc);
+    *use = 0;
+    if (!tma_store_on() || g.beta != 0.0f || splits > 1 || !aligned16(g.C) || (g.ldc * 4) % 16 ||
+        (g.batch > 1 && (g.sc * 4) % 16))
+        return KP_OK;
+    kp_status st = make_map(mc, false, g.C, g.n, g.m, g.batch, g.ldc, g.sc, 32, 32,
+                            int(CU_TENSOR_MAP_SWIZZLE_128B));
+    if (st != KP_OK) return st;
+    *use = 1;
+    return KP_OK;
+}
+
 template <int ES, int BN, bool A_MN, bool B_MN, int NBUF>
 static kp_status launch_t(const GemmProblem& g, int want_stages, cudaStream_t stream) {
     int stages = want_stages;
@@ -887,9 +1097,11 @@ static kp_status launch_t(const GemmProblem& g, int want_stages, cudaStream_t st
     p.group_m = group_m();
     p.ws = nullptr;
     if (p.splits > 1 && (st = ws_reserve(&p.ws)) != KP_OK) return st;
+    CUtensorMap mc;
+    if ((st = c_map(g, p.splits, &mc, &p.tma_store)) != KP_OK) return st;
     const int64_t units = tiles * p.splits;
     const int64_t grid = NBUF == 2 ? std::min<int64_t>(units, sm_count()) : units;
-    kern<<<dim3(unsigned(grid)), NUM_THREADS, smem, stream>>>(ma, mb, p);
+    kern<<<dim3(unsigned(grid)), NUM_THREADS, smem, stream>>>(ma, mb, mc, p);
     note_launch();
     if ((st = check_launch("tc_gemm_kernel")) != KP_OK || p.splits == 1) return st;
     // split-K: reduce the partials (programmatic dependent launch)
@@ -910,8 +1122,7 @@ static kp_status launch_t(const GemmProblem& g, int want_stages, cudaStream_t st
 }
 
 static size_t pair_smem_bytes(int bn, int stages) {
-    return STAGE_ALIGN + size_t(stages) * (BM + bn / 2) * 128 + (2 * stages + 6) * 8 +
-           4 * 32 * EPI_PITCH * 4;
+    return STAGE_ALIGN + size_t(stages) * (BM + bn / 2) * 128 + EPI_BYTES + (2 * stages + 6) * 8;
 }
 
 template <int ES, int BN, bool A_MN, bool B_MN>
@@ -972,7 +1183,9 @@ static kp_status launch_pair(const GemmProblem& g, int want_stages, cudaStream_t
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (cudaLaunchKernelEx(&cfg, kern, ma, mb, p) != cudaSuccess) return check_launch("tc_gemm_pair_kernel");
+    CUtensorMap mc;
+    if ((st = c_map(g, 1, &mc, &p.tma_store)) != KP_OK) return st;
+    if (cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, p) != cudaSuccess) return check_launch("tc_gemm_pair_kernel");
     note_launch();
     return check_launch("tc_gemm_pair_kernel");
 }
@@ -1127,3 +1340,15 @@ kp_status launch(kp_family fam, const kp_config& c, const GemmProblem& g, cudaSt
 
 }  // namespace tc
 }  // namespace kp
+
+#ifdef KP_TC_DEBUG
+// Phase timestamps of the last traced launch (KP_TC_DEBUG builds only; not
+// part of include/kp_abi.h): rows of 8 ns timestamps for CTAs 0..n-1.
+extern "C" int kp_tc_trace_dump(unsigned long long* out, int n) {
+    if (!out || n < 1 || n > kp::tc::TRACE_CTAS) return -1;
+    if (cudaMemcpyFromSymbol(out, kp::tc::g_tc_trace, size_t(n) * 16 * sizeof(unsigned long long)) !=
+        cudaSuccess)
+        return -1;
+    return 0;
+}
+#endif
