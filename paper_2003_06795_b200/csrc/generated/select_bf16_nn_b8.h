@@ -15,115 +15,90 @@ static inline select_bf16_nn_b8_config select_bf16_nn_b8(int64_t m, int64_t k, i
     (void)m;
     (void)k;
     (void)n;
-    if (k < INT64_C(1087)) {
-        if (n < INT64_C(287)) {
-            if (m < INT64_C(6272)) {
-                if (n < INT64_C(222)) {
-                    if (n < INT64_C(136)) {
-                        if (k < INT64_C(314)) {
-                            if (m < INT64_C(1569)) {
-                                if (k < INT64_C(167)) {
-                                    if (m < INT64_C(91)) {
-                                        select_bf16_nn_b8_config out = {2u, 1u, 1u, 8u, 8u};
-                                        return out;
-                                    } else {
-                                        select_bf16_nn_b8_config out = {2u, 1u, 1u, 16u, 16u};
-                                        return out;
-                                    }
-                                } else {
-                                    select_bf16_nn_b8_config out = {2u, 1u, 1u, 8u, 8u};
-                                    return out;
-                                }
-                            } else {
-                                if (k < INT64_C(96)) {
-                                    select_bf16_nn_b8_config out = {1u, 1u, 2u, 8u, 8u};
-                                    return out;
-                                } else {
-                                    select_bf16_nn_b8_config out = {1u, 1u, 1u, 8u, 8u};
-                                    return out;
-                                }
-                            }
-                        } else {
-                            if (k < INT64_C(544)) {
-                                select_bf16_nn_b8_config out = {1u, 1u, 1u, 8u, 8u};
-                                return out;
-                            } else {
-                                select_bf16_nn_b8_config out = {2u, 1u, 1u, 8u, 8u};
-                                return out;
-                            }
-                        }
-                    } else {
-                        select_bf16_nn_b8_config out = {1u, 1u, 1u, 8u, 8u};
-                        return out;
-                    }
-                } else {
-                    select_bf16_nn_b8_config out = {2u, 1u, 1u, 8u, 8u};
-                    return out;
-                }
-            } else {
-                if (n < INT64_C(79)) {
-                    select_bf16_nn_b8_config out = {1u, 1u, 2u, 8u, 8u};
+    if (k < INT64_C(2173)) {
+        if (m < INT64_C(6272)) {
+            if (k < INT64_C(79)) {
+                if (m < INT64_C(224)) {
+                    select_bf16_nn_b8_config out = {4u, 1u, 8u, 16u, 16u};
                     return out;
                 } else {
-                    if (k < INT64_C(96)) {
-                        select_bf16_nn_b8_config out = {1u, 1u, 4u, 8u, 8u};
+                    if (k < INT64_C(28)) {
+                        select_bf16_nn_b8_config out = {4u, 1u, 8u, 16u, 16u};
                         return out;
                     } else {
                         select_bf16_nn_b8_config out = {4u, 1u, 4u, 16u, 16u};
                         return out;
                     }
                 }
-            }
-        } else {
-            if (m < INT64_C(634)) {
-                if (k < INT64_C(124)) {
-                    select_bf16_nn_b8_config out = {1u, 1u, 1u, 16u, 16u};
-                    return out;
-                } else {
-                    if (k < INT64_C(992)) {
-                        if (k < INT64_C(405)) {
-                            if (k < INT64_C(227)) {
-                                select_bf16_nn_b8_config out = {1u, 1u, 2u, 8u, 8u};
+            } else {
+                if (n < INT64_C(405)) {
+                    if (m < INT64_C(1569)) {
+                        if (n < INT64_C(111)) {
+                            if (k < INT64_C(471)) {
+                                select_bf16_nn_b8_config out = {2u, 1u, 1u, 8u, 8u};
                                 return out;
                             } else {
-                                select_bf16_nn_b8_config out = {1u, 1u, 1u, 8u, 8u};
+                                select_bf16_nn_b8_config out = {2u, 2u, 4u, 16u, 16u};
                                 return out;
                             }
                         } else {
-                            select_bf16_nn_b8_config out = {1u, 1u, 2u, 8u, 8u};
+                            select_bf16_nn_b8_config out = {2u, 1u, 1u, 8u, 8u};
                             return out;
                         }
                     } else {
-                        select_bf16_nn_b8_config out = {2u, 1u, 4u, 8u, 8u};
+                        if (k < INT64_C(408)) {
+                            select_bf16_nn_b8_config out = {2u, 1u, 1u, 8u, 8u};
+                            return out;
+                        } else {
+                            select_bf16_nn_b8_config out = {4u, 1u, 8u, 16u, 16u};
+                            return out;
+                        }
+                    }
+                } else {
+                    if (m < INT64_C(634)) {
+                        if (k < INT64_C(227)) {
+                            select_bf16_nn_b8_config out = {2u, 1u, 1u, 8u, 8u};
+                            return out;
+                        } else {
+                            if (k < INT64_C(725)) {
+                                select_bf16_nn_b8_config out = {4u, 1u, 4u, 16u, 16u};
+                                return out;
+                            } else {
+                                if (k < INT64_C(1449)) {
+                                    select_bf16_nn_b8_config out = {2u, 1u, 1u, 8u, 8u};
+                                    return out;
+                                } else {
+                                    select_bf16_nn_b8_config out = {4u, 1u, 4u, 16u, 16u};
+                                    return out;
+                                }
+                            }
+                        }
+                    } else {
+                        select_bf16_nn_b8_config out = {4u, 1u, 8u, 16u, 16u};
                         return out;
                     }
                 }
+            }
+        } else {
+            if (n < INT64_C(79)) {
+                select_bf16_nn_b8_config out = {2u, 2u, 4u, 16u, 16u};
+                return out;
             } else {
-                select_bf16_nn_b8_config out = {1u, 1u, 4u, 8u, 8u};
+                select_bf16_nn_b8_config out = {4u, 1u, 4u, 16u, 16u};
                 return out;
             }
         }
     } else {
-        if (m < INT64_C(1569)) {
-            if (m < INT64_C(393)) {
-                if (n < INT64_C(363)) {
-                    select_bf16_nn_b8_config out = {2u, 1u, 4u, 8u, 8u};
-                    return out;
-                } else {
-                    select_bf16_nn_b8_config out = {4u, 1u, 4u, 16u, 16u};
-                    return out;
-                }
+        if (n < INT64_C(363)) {
+            if (m < INT64_C(785)) {
+                select_bf16_nn_b8_config out = {4u, 1u, 4u, 16u, 16u};
+                return out;
             } else {
-                if (k < INT64_C(1630)) {
-                    select_bf16_nn_b8_config out = {2u, 1u, 1u, 8u, 8u};
-                    return out;
-                } else {
-                    select_bf16_nn_b8_config out = {1u, 1u, 4u, 8u, 8u};
-                    return out;
-                }
+                select_bf16_nn_b8_config out = {4u, 1u, 8u, 16u, 16u};
+                return out;
             }
         } else {
-            select_bf16_nn_b8_config out = {4u, 1u, 4u, 16u, 16u};
+            select_bf16_nn_b8_config out = {4u, 1u, 8u, 16u, 16u};
             return out;
         }
     }

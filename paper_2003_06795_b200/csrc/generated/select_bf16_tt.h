@@ -16,522 +16,407 @@ static inline select_bf16_tt_config select_bf16_tt(int64_t m, int64_t k, int64_t
     (void)k;
     (void)n;
     if (k < INT64_C(1087)) {
-        if (m < INT64_C(8870)) {
-            if (n < INT64_C(992)) {
-                if (n < INT64_C(744)) {
-                    if (n < INT64_C(28)) {
-                        if (m < INT64_C(4435)) {
-                            if (k < INT64_C(118)) {
-                                select_bf16_tt_config out = {4u, 1u, 1u, 16u, 16u};
+        if (k < INT64_C(351)) {
+            if (n < INT64_C(222)) {
+                if (m < INT64_C(8870)) {
+                    if (n < INT64_C(46)) {
+                        if (k < INT64_C(118)) {
+                            if (m < INT64_C(4435)) {
+                                select_bf16_tt_config out = {2u, 1u, 8u, 16u, 16u};
                                 return out;
                             } else {
-                                select_bf16_tt_config out = {4u, 1u, 1u, 8u, 8u};
+                                select_bf16_tt_config out = {2u, 1u, 1u, 8u, 8u};
                                 return out;
                             }
                         } else {
-                            select_bf16_tt_config out = {4u, 1u, 1u, 16u, 16u};
-                            return out;
-                        }
-                    } else {
-                        if (m < INT64_C(2218)) {
-                            if (k < INT64_C(314)) {
-                                if (k < INT64_C(46)) {
-                                    select_bf16_tt_config out = {2u, 1u, 1u, 8u, 8u};
-                                    return out;
-                                } else {
-                                    if (n < INT64_C(46)) {
-                                        if (m < INT64_C(1109)) {
-                                            select_bf16_tt_config out = {4u, 1u, 1u, 16u, 16u};
-                                            return out;
-                                        } else {
-                                            if (k < INT64_C(167)) {
-                                                select_bf16_tt_config out = {4u, 1u, 1u, 8u, 8u};
-                                                return out;
-                                            } else {
-                                                select_bf16_tt_config out = {2u, 1u, 1u, 8u, 8u};
-                                                return out;
-                                            }
-                                        }
-                                    } else {
-                                        if (n < INT64_C(544)) {
-                                            if (n < INT64_C(444)) {
-                                                if (n < INT64_C(91)) {
-                                                    select_bf16_tt_config out = {4u, 1u, 1u, 8u, 8u};
-                                                    return out;
-                                                } else {
-                                                    if (m < INT64_C(159)) {
-                                                        select_bf16_tt_config out = {4u, 1u, 1u, 8u, 8u};
-                                                        return out;
-                                                    } else {
-                                                        if (m < INT64_C(393)) {
-                                                            select_bf16_tt_config out = {4u, 1u, 1u, 16u, 16u};
-                                                            return out;
-                                                        } else {
-                                                            if (m < INT64_C(1109)) {
-                                                                select_bf16_tt_config out = {4u, 1u, 1u, 8u, 8u};
-                                                                return out;
-                                                            } else {
-                                                                if (k < INT64_C(128)) {
-                                                                    select_bf16_tt_config out = {4u, 1u, 1u, 8u, 8u};
-                                                                    return out;
-                                                                } else {
-                                                                    select_bf16_tt_config out = {4u, 1u, 1u, 16u, 16u};
-                                                                    return out;
-                                                                }
-                                                            }
-                                                        }
-                                                    }
-                                                }
-                                            } else {
-                                                select_bf16_tt_config out = {4u, 1u, 1u, 8u, 8u};
-                                                return out;
-                                            }
-                                        } else {
-                                            if (m < INT64_C(278)) {
-                                                select_bf16_tt_config out = {2u, 1u, 1u, 8u, 8u};
-                                                return out;
-                                            } else {
-                                                if (m < INT64_C(784)) {
-                                                    select_bf16_tt_config out = {4u, 1u, 1u, 16u, 16u};
-                                                    return out;
-                                                } else {
-                                                    select_bf16_tt_config out = {4u, 1u, 1u, 8u, 8u};
-                                                    return out;
-                                                }
-                                            }
-                                        }
-                                    }
-                                }
-                            } else {
+                            if (m < INT64_C(2218)) {
                                 if (m < INT64_C(1109)) {
-                                    if (n < INT64_C(203)) {
-                                        if (m < INT64_C(555)) {
-                                            if (m < INT64_C(70)) {
-                                                select_bf16_tt_config out = {2u, 1u, 1u, 8u, 8u};
-                                                return out;
-                                            } else {
-                                                if (m < INT64_C(139)) {
-                                                    if (k < INT64_C(744)) {
-                                                        select_bf16_tt_config out = {4u, 1u, 1u, 8u, 8u};
-                                                        return out;
-                                                    } else {
-                                                        select_bf16_tt_config out = {1u, 1u, 1u, 8u, 8u};
-                                                        return out;
-                                                    }
-                                                } else {
-                                                    if (n < INT64_C(124)) {
-                                                        if (m < INT64_C(278)) {
-                                                            select_bf16_tt_config out = {4u, 1u, 1u, 8u, 8u};
-                                                            return out;
-                                                        } else {
-                                                            if (k < INT64_C(471)) {
-                                                                if (n < INT64_C(79)) {
-                                                                    select_bf16_tt_config out = {4u, 1u, 1u, 16u, 16u};
-                                                                    return out;
-                                                                } else {
-                                                                    select_bf16_tt_config out = {4u, 1u, 1u, 8u, 8u};
-                                                                    return out;
-                                                                }
-                                                            } else {
-                                                                select_bf16_tt_config out = {4u, 1u, 1u, 16u, 16u};
-                                                                return out;
-                                                            }
-                                                        }
-                                                    } else {
-                                                        if (m < INT64_C(278)) {
-                                                            select_bf16_tt_config out = {4u, 1u, 1u, 16u, 16u};
-                                                            return out;
-                                                        } else {
-                                                            if (k < INT64_C(744)) {
-                                                                select_bf16_tt_config out = {4u, 1u, 1u, 16u, 16u};
-                                                                return out;
-                                                            } else {
-                                                                select_bf16_tt_config out = {4u, 1u, 1u, 8u, 8u};
-                                                                return out;
-                                                            }
-                                                        }
-                                                    }
-                                                }
-                                            }
-                                        } else {
-                                            if (k < INT64_C(544)) {
-                                                if (k < INT64_C(444)) {
-                                                    select_bf16_tt_config out = {1u, 1u, 1u, 8u, 8u};
-                                                    return out;
-                                                } else {
-                                                    select_bf16_tt_config out = {4u, 1u, 1u, 8u, 8u};
-                                                    return out;
-                                                }
-                                            } else {
-                                                select_bf16_tt_config out = {2u, 1u, 1u, 8u, 8u};
-                                                return out;
-                                            }
-                                        }
-                                    } else {
-                                        if (m < INT64_C(278)) {
-                                            if (n < INT64_C(405)) {
-                                                if (m < INT64_C(139)) {
-                                                    if (m < INT64_C(70)) {
-                                                        select_bf16_tt_config out = {4u, 1u, 1u, 8u, 8u};
-                                                        return out;
-                                                    } else {
-                                                        select_bf16_tt_config out = {4u, 1u, 1u, 16u, 16u};
-                                                        return out;
-                                                    }
-                                                } else {
-                                                    select_bf16_tt_config out = {2u, 1u, 1u, 8u, 8u};
-                                                    return out;
-                                                }
-                                            } else {
-                                                if (m < INT64_C(70)) {
-                                                    select_bf16_tt_config out = {2u, 1u, 1u, 8u, 8u};
-                                                    return out;
-                                                } else {
-                                                    select_bf16_tt_config out = {1u, 1u, 1u, 8u, 8u};
-                                                    return out;
-                                                }
-                                            }
-                                        } else {
-                                            if (k < INT64_C(702)) {
-                                                if (n < INT64_C(363)) {
-                                                    select_bf16_tt_config out = {2u, 1u, 1u, 8u, 8u};
-                                                    return out;
-                                                } else {
-                                                    select_bf16_tt_config out = {4u, 1u, 1u, 8u, 8u};
-                                                    return out;
-                                                }
-                                            } else {
-                                                if (n < INT64_C(405)) {
-                                                    if (m < INT64_C(555)) {
-                                                        select_bf16_tt_config out = {4u, 1u, 1u, 8u, 8u};
-                                                        return out;
-                                                    } else {
-                                                        if (k < INT64_C(992)) {
-                                                            select_bf16_tt_config out = {1u, 1u, 2u, 8u, 8u};
-                                                            return out;
-                                                        } else {
-                                                            select_bf16_tt_config out = {4u, 1u, 1u, 8u, 8u};
-                                                            return out;
-                                                        }
-                                                    }
-                                                } else {
-                                                    select_bf16_tt_config out = {2u, 1u, 1u, 8u, 8u};
-                                                    return out;
-                                                }
-                                            }
-                                        }
-                                    }
-                                } else {
-                                    if (k < INT64_C(544)) {
-                                        if (n < INT64_C(79)) {
-                                            select_bf16_tt_config out = {4u, 1u, 1u, 16u, 16u};
-                                            return out;
-                                        } else {
-                                            select_bf16_tt_config out = {1u, 1u, 1u, 8u, 8u};
-                                            return out;
-                                        }
-                                    } else {
-                                        if (k < INT64_C(768)) {
-                                            select_bf16_tt_config out = {2u, 1u, 1u, 8u, 8u};
-                                            return out;
-                                        } else {
-                                            select_bf16_tt_config out = {1u, 1u, 2u, 8u, 8u};
-                                            return out;
-                                        }
-                                    }
-                                }
-                            }
-                        } else {
-                            if (n < INT64_C(363)) {
-                                if (k < INT64_C(222)) {
-                                    if (n < INT64_C(167)) {
-                                        if (n < INT64_C(46)) {
-                                            if (m < INT64_C(4435)) {
-                                                if (k < INT64_C(167)) {
-                                                    select_bf16_tt_config out = {1u, 1u, 1u, 8u, 8u};
-                                                    return out;
-                                                } else {
-                                                    select_bf16_tt_config out = {4u, 1u, 1u, 8u, 8u};
-                                                    return out;
-                                                }
-                                            } else {
-                                                if (k < INT64_C(167)) {
-                                                    select_bf16_tt_config out = {4u, 1u, 1u, 8u, 8u};
-                                                    return out;
-                                                } else {
-                                                    select_bf16_tt_config out = {4u, 1u, 1u, 16u, 16u};
-                                                    return out;
-                                                }
-                                            }
-                                        } else {
-                                            if (k < INT64_C(111)) {
-                                                if (m < INT64_C(4435)) {
-                                                    select_bf16_tt_config out = {4u, 1u, 1u, 16u, 16u};
-                                                    return out;
-                                                } else {
-                                                    if (k < INT64_C(40)) {
-                                                        select_bf16_tt_config out = {2u, 1u, 1u, 8u, 8u};
-                                                        return out;
-                                                    } else {
-                                                        select_bf16_tt_config out = {4u, 1u, 1u, 16u, 16u};
-                                                        return out;
-                                                    }
-                                                }
-                                            } else {
-                                                select_bf16_tt_config out = {2u, 1u, 1u, 8u, 8u};
-                                                return out;
-                                            }
-                                        }
-                                    } else {
-                                        if (m < INT64_C(4435)) {
-                                            select_bf16_tt_config out = {4u, 1u, 1u, 8u, 8u};
-                                            return out;
-                                        } else {
-                                            select_bf16_tt_config out = {1u, 1u, 1u, 8u, 8u};
-                                            return out;
-                                        }
-                                    }
-                                } else {
-                                    if (k < INT64_C(444)) {
-                                        if (n < INT64_C(79)) {
-                                            select_bf16_tt_config out = {1u, 1u, 1u, 8u, 8u};
-                                            return out;
-                                        } else {
-                                            if (m < INT64_C(4435)) {
-                                                if (k < INT64_C(314)) {
-                                                    select_bf16_tt_config out = {1u, 1u, 1u, 8u, 8u};
-                                                    return out;
-                                                } else {
-                                                    select_bf16_tt_config out = {2u, 1u, 1u, 8u, 8u};
-                                                    return out;
-                                                }
-                                            } else {
-                                                select_bf16_tt_config out = {2u, 1u, 1u, 8u, 8u};
-                                                return out;
-                                            }
-                                        }
-                                    } else {
-                                        if (n < INT64_C(79)) {
-                                            select_bf16_tt_config out = {2u, 1u, 1u, 8u, 8u};
-                                            return out;
-                                        } else {
-                                            if (n < INT64_C(182)) {
-                                                if (m < INT64_C(4435)) {
-                                                    if (k < INT64_C(544)) {
-                                                        select_bf16_tt_config out = {1u, 1u, 1u, 8u, 8u};
-                                                        return out;
-                                                    } else {
-                                                        select_bf16_tt_config out = {4u, 1u, 1u, 8u, 8u};
-                                                        return out;
-                                                    }
-                                                } else {
-                                                    select_bf16_tt_config out = {4u, 1u, 1u, 8u, 8u};
-                                                    return out;
-                                                }
-                                            } else {
-                                                select_bf16_tt_config out = {2u, 1u, 1u, 8u, 8u};
-                                                return out;
-                                            }
-                                        }
-                                    }
-                                }
-                            } else {
-                                if (m < INT64_C(4435)) {
-                                    if (k < INT64_C(111)) {
-                                        select_bf16_tt_config out = {1u, 1u, 2u, 8u, 8u};
-                                        return out;
-                                    } else {
-                                        select_bf16_tt_config out = {1u, 1u, 1u, 8u, 8u};
-                                        return out;
-                                    }
-                                } else {
-                                    select_bf16_tt_config out = {1u, 1u, 2u, 8u, 8u};
-                                    return out;
-                                }
-                            }
-                        }
-                    }
-                } else {
-                    select_bf16_tt_config out = {4u, 1u, 1u, 8u, 8u};
-                    return out;
-                }
-            } else {
-                if (m < INT64_C(555)) {
-                    if (n < INT64_C(1620)) {
-                        if (m < INT64_C(139)) {
-                            select_bf16_tt_config out = {4u, 1u, 1u, 16u, 16u};
-                            return out;
-                        } else {
-                            if (k < INT64_C(287)) {
-                                select_bf16_tt_config out = {4u, 1u, 1u, 16u, 16u};
-                                return out;
-                            } else {
-                                if (m < INT64_C(278)) {
-                                    select_bf16_tt_config out = {4u, 1u, 1u, 8u, 8u};
-                                    return out;
-                                } else {
-                                    if (k < INT64_C(405)) {
-                                        select_bf16_tt_config out = {1u, 1u, 1u, 8u, 8u};
-                                        return out;
-                                    } else {
-                                        select_bf16_tt_config out = {4u, 1u, 1u, 8u, 8u};
-                                        return out;
-                                    }
-                                }
-                            }
-                        }
-                    } else {
-                        if (m < INT64_C(139)) {
-                            if (k < INT64_C(725)) {
-                                select_bf16_tt_config out = {1u, 1u, 1u, 8u, 8u};
-                                return out;
-                            } else {
-                                if (m < INT64_C(70)) {
-                                    select_bf16_tt_config out = {2u, 1u, 4u, 8u, 8u};
-                                    return out;
-                                } else {
-                                    select_bf16_tt_config out = {1u, 1u, 2u, 8u, 8u};
-                                    return out;
-                                }
-                            }
-                        } else {
-                            if (m < INT64_C(278)) {
-                                if (k < INT64_C(725)) {
-                                    select_bf16_tt_config out = {2u, 1u, 1u, 8u, 8u};
-                                    return out;
-                                } else {
-                                    select_bf16_tt_config out = {4u, 1u, 1u, 16u, 16u};
-                                    return out;
-                                }
-                            } else {
-                                select_bf16_tt_config out = {1u, 1u, 2u, 8u, 8u};
-                                return out;
-                            }
-                        }
-                    }
-                } else {
-                    if (m < INT64_C(1109)) {
-                        if (k < INT64_C(405)) {
-                            select_bf16_tt_config out = {1u, 1u, 1u, 8u, 8u};
-                            return out;
-                        } else {
-                            select_bf16_tt_config out = {1u, 1u, 2u, 8u, 8u};
-                            return out;
-                        }
-                    } else {
-                        select_bf16_tt_config out = {1u, 1u, 2u, 8u, 8u};
-                        return out;
-                    }
-                }
-            }
-        } else {
-            if (n < INT64_C(46)) {
-                if (m < INT64_C(70960)) {
-                    if (m < INT64_C(35480)) {
-                        if (k < INT64_C(56)) {
-                            if (m < INT64_C(17740)) {
-                                if (k < INT64_C(30)) {
-                                    select_bf16_tt_config out = {4u, 1u, 1u, 16u, 16u};
-                                    return out;
-                                } else {
-                                    select_bf16_tt_config out = {4u, 1u, 1u, 8u, 8u};
-                                    return out;
-                                }
-                            } else {
-                                if (k < INT64_C(30)) {
-                                    select_bf16_tt_config out = {4u, 1u, 1u, 8u, 8u};
-                                    return out;
-                                } else {
-                                    select_bf16_tt_config out = {1u, 1u, 1u, 8u, 8u};
-                                    return out;
-                                }
-                            }
-                        } else {
-                            if (m < INT64_C(17740)) {
-                                if (k < INT64_C(118)) {
-                                    select_bf16_tt_config out = {1u, 1u, 1u, 8u, 8u};
+                                    select_bf16_tt_config out = {8u, 1u, 2u, 16u, 16u};
                                     return out;
                                 } else {
                                     if (k < INT64_C(167)) {
-                                        if (n < INT64_C(28)) {
-                                            select_bf16_tt_config out = {4u, 1u, 1u, 16u, 16u};
+                                        select_bf16_tt_config out = {8u, 1u, 4u, 16u, 16u};
+                                        return out;
+                                    } else {
+                                        select_bf16_tt_config out = {8u, 1u, 2u, 16u, 16u};
+                                        return out;
+                                    }
+                                }
+                            } else {
+                                if (n < INT64_C(28)) {
+                                    if (m < INT64_C(4435)) {
+                                        select_bf16_tt_config out = {8u, 1u, 4u, 16u, 16u};
+                                        return out;
+                                    } else {
+                                        select_bf16_tt_config out = {8u, 1u, 2u, 16u, 16u};
+                                        return out;
+                                    }
+                                } else {
+                                    select_bf16_tt_config out = {1u, 1u, 4u, 8u, 8u};
+                                    return out;
+                                }
+                            }
+                        }
+                    } else {
+                        if (m < INT64_C(2218)) {
+                            if (m < INT64_C(555)) {
+                                if (m < INT64_C(224)) {
+                                    select_bf16_tt_config out = {2u, 1u, 1u, 8u, 8u};
+                                    return out;
+                                } else {
+                                    select_bf16_tt_config out = {1u, 1u, 4u, 8u, 8u};
+                                    return out;
+                                }
+                            } else {
+                                select_bf16_tt_config out = {2u, 1u, 1u, 8u, 8u};
+                                return out;
+                            }
+                        } else {
+                            if (k < INT64_C(111)) {
+                                if (k < INT64_C(28)) {
+                                    if (m < INT64_C(4435)) {
+                                        select_bf16_tt_config out = {8u, 1u, 2u, 16u, 16u};
+                                        return out;
+                                    } else {
+                                        select_bf16_tt_config out = {2u, 1u, 1u, 8u, 8u};
+                                        return out;
+                                    }
+                                } else {
+                                    select_bf16_tt_config out = {2u, 1u, 1u, 8u, 8u};
+                                    return out;
+                                }
+                            } else {
+                                if (k < INT64_C(222)) {
+                                    select_bf16_tt_config out = {8u, 1u, 2u, 16u, 16u};
+                                    return out;
+                                } else {
+                                    if (m < INT64_C(4435)) {
+                                        select_bf16_tt_config out = {2u, 1u, 1u, 8u, 8u};
+                                        return out;
+                                    } else {
+                                        if (n < INT64_C(91)) {
+                                            select_bf16_tt_config out = {2u, 1u, 1u, 8u, 8u};
                                             return out;
                                         } else {
-                                            select_bf16_tt_config out = {4u, 1u, 1u, 8u, 8u};
+                                            select_bf16_tt_config out = {8u, 1u, 2u, 16u, 16u};
+                                            return out;
+                                        }
+                                    }
+                                }
+                            }
+                        }
+                    }
+                } else {
+                    if (n < INT64_C(46)) {
+                        if (k < INT64_C(30)) {
+                            if (m < INT64_C(17740)) {
+                                select_bf16_tt_config out = {8u, 1u, 4u, 16u, 16u};
+                                return out;
+                            } else {
+                                if (m < INT64_C(70960)) {
+                                    select_bf16_tt_config out = {2u, 1u, 1u, 8u, 8u};
+                                    return out;
+                                } else {
+                                    if (m < INT64_C(141920)) {
+                                        select_bf16_tt_config out = {8u, 2u, 8u, 16u, 16u};
+                                        return out;
+                                    } else {
+                                        select_bf16_tt_config out = {2u, 1u, 1u, 8u, 8u};
+                                        return out;
+                                    }
+                                }
+                            }
+                        } else {
+                            if (m < INT64_C(35480)) {
+                                if (k < INT64_C(167)) {
+                                    if (m < INT64_C(17740)) {
+                                        if (k < INT64_C(118)) {
+                                            if (k < INT64_C(56)) {
+                                                select_bf16_tt_config out = {8u, 1u, 2u, 16u, 16u};
+                                                return out;
+                                            } else {
+                                                select_bf16_tt_config out = {1u, 1u, 4u, 8u, 8u};
+                                                return out;
+                                            }
+                                        } else {
+                                            select_bf16_tt_config out = {2u, 1u, 1u, 8u, 8u};
                                             return out;
                                         }
                                     } else {
                                         select_bf16_tt_config out = {2u, 1u, 1u, 8u, 8u};
                                         return out;
                                     }
+                                } else {
+                                    select_bf16_tt_config out = {8u, 1u, 2u, 16u, 16u};
+                                    return out;
                                 }
+                            } else {
+                                select_bf16_tt_config out = {8u, 1u, 2u, 16u, 16u};
+                                return out;
+                            }
+                        }
+                    } else {
+                        if (k < INT64_C(20)) {
+                            if (m < INT64_C(70960)) {
+                                select_bf16_tt_config out = {8u, 1u, 4u, 16u, 16u};
+                                return out;
+                            } else {
+                                select_bf16_tt_config out = {1u, 1u, 4u, 8u, 8u};
+                                return out;
+                            }
+                        } else {
+                            if (m < INT64_C(283839)) {
+                                if (k < INT64_C(194)) {
+                                    if (k < INT64_C(28)) {
+                                        if (m < INT64_C(35480)) {
+                                            select_bf16_tt_config out = {8u, 2u, 8u, 16u, 16u};
+                                            return out;
+                                        } else {
+                                            select_bf16_tt_config out = {8u, 1u, 2u, 16u, 16u};
+                                            return out;
+                                        }
+                                    } else {
+                                        if (m < INT64_C(17740)) {
+                                            if (k < INT64_C(46)) {
+                                                select_bf16_tt_config out = {8u, 1u, 2u, 16u, 16u};
+                                                return out;
+                                            } else {
+                                                if (k < INT64_C(97)) {
+                                                    select_bf16_tt_config out = {2u, 1u, 8u, 16u, 16u};
+                                                    return out;
+                                                } else {
+                                                    select_bf16_tt_config out = {8u, 1u, 2u, 16u, 16u};
+                                                    return out;
+                                                }
+                                            }
+                                        } else {
+                                            select_bf16_tt_config out = {8u, 1u, 2u, 16u, 16u};
+                                            return out;
+                                        }
+                                    }
+                                } else {
+                                    if (m < INT64_C(17740)) {
+                                        if (n < INT64_C(91)) {
+                                            select_bf16_tt_config out = {8u, 1u, 2u, 16u, 16u};
+                                            return out;
+                                        } else {
+                                            select_bf16_tt_config out = {8u, 2u, 8u, 16u, 16u};
+                                            return out;
+                                        }
+                                    } else {
+                                        if (m < INT64_C(35480)) {
+                                            select_bf16_tt_config out = {1u, 1u, 4u, 8u, 8u};
+                                            return out;
+                                        } else {
+                                            select_bf16_tt_config out = {8u, 2u, 8u, 16u, 16u};
+                                            return out;
+                                        }
+                                    }
+                                }
+                            } else {
+                                if (m < INT64_C(567677)) {
+                                    select_bf16_tt_config out = {1u, 1u, 4u, 8u, 8u};
+                                    return out;
+                                } else {
+                                    select_bf16_tt_config out = {8u, 2u, 8u, 16u, 16u};
+                                    return out;
+                                }
+                            }
+                        }
+                    }
+                }
+            } else {
+                if (m < INT64_C(2218)) {
+                    if (k < INT64_C(79)) {
+                        if (m < INT64_C(555)) {
+                            select_bf16_tt_config out = {1u, 1u, 4u, 8u, 8u};
+                            return out;
+                        } else {
+                            select_bf16_tt_config out = {8u, 1u, 4u, 16u, 16u};
+                            return out;
+                        }
+                    } else {
+                        if (m < INT64_C(1109)) {
+                            if (n < INT64_C(744)) {
+                                if (m < INT64_C(278)) {
+                                    select_bf16_tt_config out = {8u, 1u, 2u, 16u, 16u};
+                                    return out;
+                                } else {
+                                    if (m < INT64_C(555)) {
+                                        select_bf16_tt_config out = {2u, 1u, 1u, 8u, 8u};
+                                        return out;
+                                    } else {
+                                        if (k < INT64_C(182)) {
+                                            select_bf16_tt_config out = {8u, 1u, 2u, 16u, 16u};
+                                            return out;
+                                        } else {
+                                            select_bf16_tt_config out = {2u, 1u, 1u, 8u, 8u};
+                                            return out;
+                                        }
+                                    }
+                                }
+                            } else {
+                                if (m < INT64_C(278)) {
+                                    if (m < INT64_C(70)) {
+                                        select_bf16_tt_config out = {8u, 1u, 2u, 16u, 16u};
+                                        return out;
+                                    } else {
+                                        if (m < INT64_C(139)) {
+                                            if (k < INT64_C(227)) {
+                                                select_bf16_tt_config out = {2u, 1u, 1u, 8u, 8u};
+                                                return out;
+                                            } else {
+                                                select_bf16_tt_config out = {8u, 1u, 2u, 16u, 16u};
+                                                return out;
+                                            }
+                                        } else {
+                                            if (k < INT64_C(287)) {
+                                                select_bf16_tt_config out = {8u, 1u, 2u, 16u, 16u};
+                                                return out;
+                                            } else {
+                                                select_bf16_tt_config out = {2u, 1u, 1u, 8u, 8u};
+                                                return out;
+                                            }
+                                        }
+                                    }
+                                } else {
+                                    select_bf16_tt_config out = {8u, 1u, 2u, 16u, 16u};
+                                    return out;
+                                }
+                            }
+                        } else {
+                            if (n < INT64_C(768)) {
+                                select_bf16_tt_config out = {8u, 1u, 2u, 16u, 16u};
+                                return out;
+                            } else {
+                                select_bf16_tt_config out = {8u, 1u, 4u, 16u, 16u};
+                                return out;
+                            }
+                        }
+                    }
+                } else {
+                    if (m < INT64_C(35480)) {
+                        if (n < INT64_C(768)) {
+                            if (m < INT64_C(4435)) {
+                                select_bf16_tt_config out = {8u, 1u, 4u, 16u, 16u};
+                                return out;
+                            } else {
+                                if (k < INT64_C(182)) {
+                                    if (m < INT64_C(8870)) {
+                                        select_bf16_tt_config out = {1u, 1u, 4u, 8u, 8u};
+                                        return out;
+                                    } else {
+                                        if (m < INT64_C(17740)) {
+                                            if (k < INT64_C(91)) {
+                                                select_bf16_tt_config out = {2u, 1u, 8u, 16u, 16u};
+                                                return out;
+                                            } else {
+                                                select_bf16_tt_config out = {8u, 1u, 4u, 16u, 16u};
+                                                return out;
+                                            }
+                                        } else {
+                                            select_bf16_tt_config out = {8u, 1u, 4u, 16u, 16u};
+                                            return out;
+                                        }
+                                    }
+                                } else {
+                                    select_bf16_tt_config out = {2u, 1u, 8u, 16u, 16u};
+                                    return out;
+                                }
+                            }
+                        } else {
+                            select_bf16_tt_config out = {1u, 1u, 4u, 8u, 8u};
+                            return out;
+                        }
+                    } else {
+                        select_bf16_tt_config out = {8u, 2u, 8u, 16u, 16u};
+                        return out;
+                    }
+                }
+            }
+        } else {
+            if (m < INT64_C(4435)) {
+                if (n < INT64_C(725)) {
+                    if (k < INT64_C(992)) {
+                        select_bf16_tt_config out = {2u, 1u, 1u, 8u, 8u};
+                        return out;
+                    } else {
+                        if (m < INT64_C(278)) {
+                            select_bf16_tt_config out = {2u, 1u, 1u, 8u, 8u};
+                            return out;
+                        } else {
+                            if (m < INT64_C(1109)) {
+                                select_bf16_tt_config out = {8u, 1u, 2u, 16u, 16u};
+                                return out;
                             } else {
                                 select_bf16_tt_config out = {2u, 1u, 1u, 8u, 8u};
                                 return out;
                             }
                         }
-                    } else {
-                        if (k < INT64_C(51)) {
-                            select_bf16_tt_config out = {4u, 1u, 1u, 16u, 16u};
-                            return out;
-                        } else {
-                            if (k < INT64_C(118)) {
-                                select_bf16_tt_config out = {1u, 1u, 1u, 8u, 8u};
-                                return out;
-                            } else {
-                                select_bf16_tt_config out = {4u, 1u, 1u, 16u, 16u};
-                                return out;
-                            }
-                        }
                     }
                 } else {
-                    select_bf16_tt_config out = {1u, 1u, 1u, 8u, 8u};
-                    return out;
-                }
-            } else {
-                if (m < INT64_C(35480)) {
-                    if (n < INT64_C(111)) {
-                        if (m < INT64_C(17740)) {
-                            if (k < INT64_C(194)) {
-                                select_bf16_tt_config out = {4u, 1u, 1u, 8u, 8u};
+                    if (m < INT64_C(555)) {
+                        if (k < INT64_C(725)) {
+                            if (m < INT64_C(278)) {
+                                select_bf16_tt_config out = {2u, 1u, 1u, 8u, 8u};
                                 return out;
                             } else {
-                                if (k < INT64_C(384)) {
+                                if (n < INT64_C(1449)) {
                                     select_bf16_tt_config out = {2u, 1u, 1u, 8u, 8u};
                                     return out;
                                 } else {
-                                    select_bf16_tt_config out = {4u, 1u, 1u, 8u, 8u};
+                                    select_bf16_tt_config out = {8u, 1u, 2u, 16u, 16u};
                                     return out;
                                 }
                             }
                         } else {
-                            if (k < INT64_C(49)) {
-                                select_bf16_tt_config out = {1u, 1u, 1u, 8u, 8u};
+                            if (m < INT64_C(70)) {
+                                select_bf16_tt_config out = {8u, 1u, 4u, 16u, 16u};
                                 return out;
                             } else {
-                                if (k < INT64_C(194)) {
-                                    select_bf16_tt_config out = {4u, 1u, 1u, 16u, 16u};
+                                if (m < INT64_C(139)) {
+                                    select_bf16_tt_config out = {1u, 1u, 4u, 8u, 8u};
                                     return out;
                                 } else {
-                                    select_bf16_tt_config out = {1u, 1u, 2u, 8u, 8u};
+                                    select_bf16_tt_config out = {2u, 1u, 1u, 8u, 8u};
                                     return out;
                                 }
                             }
                         }
                     } else {
-                        select_bf16_tt_config out = {1u, 1u, 2u, 8u, 8u};
+                        if (m < INT64_C(1568)) {
+                            select_bf16_tt_config out = {8u, 1u, 4u, 16u, 16u};
+                            return out;
+                        } else {
+                            select_bf16_tt_config out = {2u, 1u, 8u, 16u, 16u};
+                            return out;
+                        }
+                    }
+                }
+            } else {
+                if (n < INT64_C(91)) {
+                    if (m < INT64_C(8870)) {
+                        select_bf16_tt_config out = {2u, 1u, 1u, 8u, 8u};
+                        return out;
+                    } else {
+                        select_bf16_tt_config out = {8u, 1u, 2u, 16u, 16u};
                         return out;
                     }
                 } else {
-                    if (n < INT64_C(111)) {
-                        select_bf16_tt_config out = {1u, 1u, 2u, 8u, 8u};
-                        return out;
-                    } else {
-                        if (m < INT64_C(70960)) {
-                            select_bf16_tt_config out = {1u, 1u, 2u, 8u, 8u};
+                    if (m < INT64_C(35480)) {
+                        if (m < INT64_C(8870)) {
+                            select_bf16_tt_config out = {8u, 1u, 2u, 16u, 16u};
                             return out;
                         } else {
-                            select_bf16_tt_config out = {8u, 1u, 8u, 16u, 16u};
+                            select_bf16_tt_config out = {1u, 1u, 4u, 8u, 8u};
+                            return out;
+                        }
+                    } else {
+                        if (m < INT64_C(141920)) {
+                            select_bf16_tt_config out = {8u, 1u, 4u, 16u, 16u};
+                            return out;
+                        } else {
+                            select_bf16_tt_config out = {8u, 2u, 8u, 16u, 16u};
                             return out;
                         }
                     }
@@ -539,171 +424,156 @@ static inline select_bf16_tt_config select_bf16_tt(int64_t m, int64_t k, int64_t
             }
         }
     } else {
-        if (m < INT64_C(1109)) {
-            if (n < INT64_C(2024)) {
-                if (m < INT64_C(278)) {
-                    if (m < INT64_C(28)) {
+        if (m < INT64_C(2509)) {
+            if (n < INT64_C(1432)) {
+                if (m < INT64_C(12)) {
+                    if (m < INT64_C(3)) {
                         if (k < INT64_C(2897)) {
-                            if (m < INT64_C(6)) {
-                                if (m < INT64_C(2)) {
-                                    select_bf16_tt_config out = {2u, 1u, 4u, 8u, 8u};
-                                    return out;
-                                } else {
-                                    select_bf16_tt_config out = {1u, 1u, 2u, 8u, 8u};
-                                    return out;
-                                }
-                            } else {
-                                if (m < INT64_C(12)) {
-                                    select_bf16_tt_config out = {1u, 1u, 2u, 8u, 8u};
-                                    return out;
-                                } else {
-                                    if (k < INT64_C(1620)) {
-                                        select_bf16_tt_config out = {1u, 1u, 2u, 8u, 8u};
-                                        return out;
-                                    } else {
-                                        select_bf16_tt_config out = {2u, 1u, 1u, 8u, 8u};
-                                        return out;
-                                    }
-                                }
-                            }
+                            select_bf16_tt_config out = {8u, 1u, 4u, 16u, 16u};
+                            return out;
                         } else {
-                            select_bf16_tt_config out = {1u, 1u, 2u, 8u, 8u};
+                            select_bf16_tt_config out = {1u, 1u, 4u, 8u, 8u};
                             return out;
                         }
                     } else {
-                        if (n < INT64_C(363)) {
-                            select_bf16_tt_config out = {1u, 1u, 1u, 8u, 8u};
-                            return out;
-                        } else {
-                            if (m < INT64_C(139)) {
-                                if (m < INT64_C(70)) {
-                                    select_bf16_tt_config out = {4u, 1u, 1u, 16u, 16u};
-                                    return out;
-                                } else {
-                                    if (k < INT64_C(3072)) {
-                                        select_bf16_tt_config out = {4u, 1u, 1u, 16u, 16u};
-                                        return out;
-                                    } else {
-                                        select_bf16_tt_config out = {2u, 1u, 1u, 8u, 8u};
-                                        return out;
-                                    }
-                                }
+                        select_bf16_tt_config out = {1u, 1u, 4u, 8u, 8u};
+                        return out;
+                    }
+                } else {
+                    if (m < INT64_C(555)) {
+                        if (k < INT64_C(4345)) {
+                            if (m < INT64_C(40)) {
+                                select_bf16_tt_config out = {8u, 1u, 2u, 16u, 16u};
+                                return out;
                             } else {
-                                if (k < INT64_C(3072)) {
+                                if (m < INT64_C(139)) {
                                     select_bf16_tt_config out = {2u, 1u, 1u, 8u, 8u};
                                     return out;
                                 } else {
-                                    select_bf16_tt_config out = {1u, 1u, 2u, 8u, 8u};
+                                    select_bf16_tt_config out = {8u, 1u, 2u, 16u, 16u};
+                                    return out;
+                                }
+                            }
+                        } else {
+                            if (m < INT64_C(70)) {
+                                select_bf16_tt_config out = {2u, 1u, 1u, 8u, 8u};
+                                return out;
+                            } else {
+                                if (m < INT64_C(139)) {
+                                    select_bf16_tt_config out = {8u, 1u, 4u, 16u, 16u};
+                                    return out;
+                                } else {
+                                    select_bf16_tt_config out = {1u, 1u, 4u, 8u, 8u};
                                     return out;
                                 }
                             }
                         }
-                    }
-                } else {
-                    if (k < INT64_C(3259)) {
-                        select_bf16_tt_config out = {2u, 1u, 4u, 8u, 8u};
-                        return out;
                     } else {
-                        select_bf16_tt_config out = {4u, 1u, 8u, 8u, 8u};
-                        return out;
+                        if (m < INT64_C(1109)) {
+                            if (n < INT64_C(363)) {
+                                select_bf16_tt_config out = {8u, 1u, 4u, 16u, 16u};
+                                return out;
+                            } else {
+                                select_bf16_tt_config out = {1u, 1u, 4u, 8u, 8u};
+                                return out;
+                            }
+                        } else {
+                            if (n < INT64_C(363)) {
+                                if (k < INT64_C(1630)) {
+                                    select_bf16_tt_config out = {8u, 1u, 2u, 16u, 16u};
+                                    return out;
+                                } else {
+                                    select_bf16_tt_config out = {1u, 1u, 4u, 8u, 8u};
+                                    return out;
+                                }
+                            } else {
+                                select_bf16_tt_config out = {2u, 1u, 8u, 16u, 16u};
+                                return out;
+                            }
+                        }
                     }
                 }
             } else {
                 if (m < INT64_C(12)) {
-                    if (m < INT64_C(3)) {
-                        if (m < INT64_C(2)) {
-                            if (k < INT64_C(10138)) {
-                                select_bf16_tt_config out = {8u, 1u, 8u, 16u, 16u};
-                                return out;
-                            } else {
-                                select_bf16_tt_config out = {4u, 1u, 8u, 8u, 8u};
-                                return out;
-                            }
+                    select_bf16_tt_config out = {2u, 1u, 8u, 16u, 16u};
+                    return out;
+                } else {
+                    if (m < INT64_C(182)) {
+                        if (k < INT64_C(10138)) {
+                            select_bf16_tt_config out = {8u, 1u, 4u, 16u, 16u};
+                            return out;
                         } else {
-                            select_bf16_tt_config out = {8u, 1u, 8u, 16u, 16u};
+                            select_bf16_tt_config out = {2u, 1u, 8u, 16u, 16u};
                             return out;
                         }
                     } else {
-                        select_bf16_tt_config out = {4u, 1u, 8u, 8u, 8u};
+                        select_bf16_tt_config out = {2u, 1u, 8u, 16u, 16u};
                         return out;
                     }
-                } else {
-                    select_bf16_tt_config out = {8u, 1u, 8u, 16u, 16u};
-                    return out;
                 }
             }
         } else {
-            if (k < INT64_C(1537)) {
-                if (m < INT64_C(35480)) {
-                    if (m < INT64_C(8870)) {
-                        if (n < INT64_C(182)) {
-                            select_bf16_tt_config out = {4u, 1u, 1u, 8u, 8u};
+            if (k < INT64_C(2661)) {
+                if (m < INT64_C(17740)) {
+                    if (n < INT64_C(182)) {
+                        if (m < INT64_C(8870)) {
+                            select_bf16_tt_config out = {2u, 1u, 1u, 8u, 8u};
                             return out;
                         } else {
-                            if (m < INT64_C(4435)) {
-                                select_bf16_tt_config out = {2u, 1u, 1u, 8u, 8u};
-                                return out;
-                            } else {
-                                select_bf16_tt_config out = {1u, 1u, 1u, 8u, 8u};
-                                return out;
-                            }
+                            select_bf16_tt_config out = {8u, 1u, 4u, 16u, 16u};
+                            return out;
                         }
                     } else {
-                        if (m < INT64_C(17740)) {
-                            if (n < INT64_C(182)) {
-                                select_bf16_tt_config out = {1u, 1u, 1u, 8u, 8u};
-                                return out;
+                        if (m < INT64_C(8870)) {
+                            if (k < INT64_C(1630)) {
+                                if (m < INT64_C(4435)) {
+                                    select_bf16_tt_config out = {8u, 1u, 2u, 16u, 16u};
+                                    return out;
+                                } else {
+                                    select_bf16_tt_config out = {8u, 1u, 4u, 16u, 16u};
+                                    return out;
+                                }
                             } else {
-                                select_bf16_tt_config out = {1u, 1u, 2u, 8u, 8u};
+                                select_bf16_tt_config out = {2u, 1u, 8u, 16u, 16u};
                                 return out;
                             }
                         } else {
-                            select_bf16_tt_config out = {1u, 1u, 2u, 8u, 8u};
-                            return out;
+                            if (n < INT64_C(363)) {
+                                select_bf16_tt_config out = {2u, 1u, 8u, 16u, 16u};
+                                return out;
+                            } else {
+                                select_bf16_tt_config out = {8u, 2u, 8u, 16u, 16u};
+                                return out;
+                            }
                         }
                     }
                 } else {
-                    select_bf16_tt_config out = {8u, 1u, 8u, 16u, 16u};
-                    return out;
+                    if (k < INT64_C(1630)) {
+                        if (m < INT64_C(35480)) {
+                            select_bf16_tt_config out = {1u, 1u, 4u, 8u, 8u};
+                            return out;
+                        } else {
+                            if (m < INT64_C(70960)) {
+                                select_bf16_tt_config out = {8u, 1u, 4u, 16u, 16u};
+                                return out;
+                            } else {
+                                if (m < INT64_C(141920)) {
+                                    select_bf16_tt_config out = {8u, 2u, 8u, 16u, 16u};
+                                    return out;
+                                } else {
+                                    select_bf16_tt_config out = {8u, 1u, 4u, 16u, 16u};
+                                    return out;
+                                }
+                            }
+                        }
+                    } else {
+                        select_bf16_tt_config out = {8u, 2u, 8u, 16u, 16u};
+                        return out;
+                    }
                 }
             } else {
-                if (n < INT64_C(1025)) {
-                    if (m < INT64_C(8870)) {
-                        if (m < INT64_C(2218)) {
-                            if (n < INT64_C(363)) {
-                                select_bf16_tt_config out = {2u, 1u, 4u, 8u, 8u};
-                                return out;
-                            } else {
-                                select_bf16_tt_config out = {8u, 1u, 8u, 16u, 16u};
-                                return out;
-                            }
-                        } else {
-                            if (k < INT64_C(3259)) {
-                                select_bf16_tt_config out = {4u, 1u, 8u, 8u, 8u};
-                                return out;
-                            } else {
-                                select_bf16_tt_config out = {4u, 1u, 8u, 8u, 8u};
-                                return out;
-                            }
-                        }
-                    } else {
-                        if (m < INT64_C(17740)) {
-                            if (n < INT64_C(363)) {
-                                select_bf16_tt_config out = {1u, 1u, 2u, 8u, 8u};
-                                return out;
-                            } else {
-                                select_bf16_tt_config out = {8u, 1u, 8u, 16u, 16u};
-                                return out;
-                            }
-                        } else {
-                            select_bf16_tt_config out = {8u, 1u, 8u, 16u, 16u};
-                            return out;
-                        }
-                    }
-                } else {
-                    select_bf16_tt_config out = {8u, 1u, 8u, 16u, 16u};
-                    return out;
-                }
+                select_bf16_tt_config out = {8u, 2u, 8u, 16u, 16u};
+                return out;
             }
         }
     }

@@ -75,7 +75,8 @@ struct TcParams {
     int a_batch, b_batch;  // 1 if the operand advances with the batch index, else 0
     int splits;            // K splits per tile (1 = no split-K)
     int group_m;           // m-tiles per raster group
-    int tma_store;         // 1: C tile stored by TMA (beta == 0, aligned C, no split-K)
+    int tma_store;         // 1: C tile stored by TMA (beta == 0, aligned C, no split-K);
+                           // 2: split-K partial tiles stored by TMA into the workspace
     float* ws;             // split-K partial tiles [tile][split][BM][BN] (splits > 1)
 };
 
@@ -494,6 +495,15 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             const int row0 = m0 + q * 32;
             const uint32_t taddr = tmem + (uint32_t(q * 32) << 16) + uint32_t(buf * BN);
             const int cols = min(BN, p.N - n0);
+            if (p.tma_store == 2) {  // split-K partial: ws tile (unit), rows q*32.., alpha later
+                epi_tma_tile(&map_c, taddr, cols, 0, q * 32, t * p.splits + u % p.splits, 1.0f,
+                             ebufs, lane, eit);
+                fence_before_sync();
+                if (lane == 0)
+                    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(acc_empty(buf))
+                                 : "memory");
+                continue;
+            }
             if (p.tma_store) {
                 epi_tma_tile(&map_c, taddr, cols, n0, row0, bz, p.alpha, ebufs, lane, eit,
                              warp == 2 && it == 0);
@@ -1042,13 +1052,27 @@ static bool tma_store_on() {
 static kp_status c_map(const GemmProblem& g, int splits, CUtensorMap* mc, int* use) {
     std::memset(mc, 0, sizeof *mc);
     *use = 0;
-    if (!tma_store_on() || g.beta != 0.0f || splits > 1 || !aligned16(g.C) || (g.ldc * 4) % 16 ||
+    if (splits > 1) return KP_OK;  // see ws_map
+    if (!tma_store_on() || g.beta != 0.0f || !aligned16(g.C) || (g.ldc * 4) % 16 ||
         (g.batch > 1 && (g.sc * 4) % 16))
         return KP_OK;
     kp_status st = make_map(mc, false, g.C, g.n, g.m, g.batch, g.ldc, g.sc, 32, 32,
                             int(CU_TENSOR_MAP_SWIZZLE_128B));
     if (st != KP_OK) return st;
     *use = 1;
+    return KP_OK;
+}
+
+// Split-K partial tiles [unit][BM][BN] of the workspace as a 3-D fp32 tensor
+// (32x32 boxes, 128B swizzle) for the TMA-store epilogue.
+static kp_status ws_map(float* ws, int bn, int64_t units, CUtensorMap* mc, int* use) {
+    std::memset(mc, 0, sizeof *mc);
+    *use = 0;
+    if (!tma_store_on()) return KP_OK;
+    kp_status st = make_map(mc, false, ws, bn, BM, units, bn, int64_t(BM) * bn, 32, 32,
+                            int(CU_TENSOR_MAP_SWIZZLE_128B));
+    if (st != KP_OK) return st;
+    *use = 2;
     return KP_OK;
 }
 
@@ -1098,8 +1122,10 @@ static kp_status launch_t(const GemmProblem& g, int want_stages, cudaStream_t st
     p.ws = nullptr;
     if (p.splits > 1 && (st = ws_reserve(&p.ws)) != KP_OK) return st;
     CUtensorMap mc;
-    if ((st = c_map(g, p.splits, &mc, &p.tma_store)) != KP_OK) return st;
     const int64_t units = tiles * p.splits;
+    if (p.splits > 1) st = ws_map(p.ws, BN, units, &mc, &p.tma_store);
+    else st = c_map(g, p.splits, &mc, &p.tma_store);
+    if (st != KP_OK) return st;
     const int64_t grid = NBUF == 2 ? std::min<int64_t>(units, sm_count()) : units;
     kern<<<dim3(unsigned(grid)), NUM_THREADS, smem, stream>>>(ma, mb, mc, p);
     note_launch();
