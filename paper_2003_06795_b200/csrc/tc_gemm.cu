@@ -245,8 +245,11 @@ template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
     asm volatile("cp.async.bulk.wait_group.read %0;" :: "n"(N) : "memory");
 }
-__device__ __forceinline__ void bulk_wait_all() {
-    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+// Before the CTA exits: its bulk stores have finished reading shared memory
+// (their global writes complete with the grid, as every kernel boundary and
+// the split-K reduce's griddepcontrol.wait observe).
+__device__ __forceinline__ void bulk_wait_smem_free() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
 // One epilogue warp stores its 32 rows x `cols` of the accumulator through
@@ -497,7 +500,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             const int cols = min(BN, p.N - n0);
             if (p.tma_store == 2) {  // split-K partial: ws tile (unit), rows q*32.., alpha later
                 epi_tma_tile(&map_c, taddr, cols, 0, q * 32, t * p.splits + u % p.splits, 1.0f,
-                             ebufs, lane, eit);
+                             ebufs, lane, eit, warp == 2 && it == 0);
+                if (warp == 2 && lane == 0) trace(6);
                 fence_before_sync();
                 if (lane == 0)
                     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(acc_empty(buf))
@@ -552,7 +556,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             }
         }
     }
-    if (p.tma_store && warp >= 2 && lane == 0) bulk_wait_all();  // stores out of smem
+    if (p.tma_store && warp >= 2 && lane == 0) bulk_wait_smem_free();
     fence_before_sync();
     __syncthreads();
     if (warp == 1) {
@@ -832,7 +836,7 @@ tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap map_a,
             }
         }
     }
-    if (p.tma_store && warp >= 2 && lane == 0) bulk_wait_all();  // stores out of smem
+    if (p.tma_store && warp >= 2 && lane == 0) bulk_wait_smem_free();
     fence_before_sync();
     __syncthreads();
     cluster_sync();
@@ -1048,7 +1052,6 @@ static bool tma_store_on() {
     }();
     return on;
 }
-
 static kp_status c_map(const GemmProblem& g, int splits, CUtensorMap* mc, int* use) {
     std::memset(mc, 0, sizeof *mc);
     *use = 0;
