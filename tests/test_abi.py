@@ -149,3 +149,37 @@ def test_batched_selector_dispatch():
             else:
                 assert cfg.as_tuple() == codegen.traverse_document(plain, m, k, n).as_tuple()
     assert lib.kp_select_ex(0, 0, 0, 0, 8, 8, 8, ctypes.byref(cfg)) == nat.KP_ERR_BAD_SHAPE
+
+
+def test_selector_variant_names_and_table():
+    """Variant keys: layout, optionally _b<batch> (one selector per (family,
+    trans, batch)); the generated table lists each with its batch."""
+    from paper_2003_06795_b200 import libgen
+    from paper_2003_06795_b200.errors import DataError
+    assert libgen.variant_batch("nn") == 1
+    assert libgen.variant_batch("tt") == 1
+    assert libgen.variant_batch("nn_b8") == 8
+    for bad in ("xx", "nn_b", "nn_8", "nnb8"):
+        with pytest.raises(DataError):
+            libgen.variant_batch(bad)
+    table = (libgen.GEN_DIR / "selectors.h").read_text()
+    for fam, trans in libgen.installed():
+        sym = libgen.symbol_for(fam, trans)
+        ta = "true" if trans[0] == "t" else "false"
+        tb = "true" if trans[1] == "t" else "false"
+        row = (f"{{{libgen.FAMILY_IDS[fam]}, {ta}, {tb}, {libgen.variant_batch(trans)}, "
+               f"kp_wrap_{sym}, \"{sym}.h\"}},")
+        assert row in table, row
+
+
+def test_skinny_config_is_not_a_kernel_config():
+    """The all-zero config names the small-M path in kp_gemm / kp_gemm_time /
+    sweeps, but kp_config_valid (the reference's KernelConfig validation)
+    still rejects it."""
+    lib = nat.lib()
+    zero = nat.to_kp_config(nat.SKINNY)
+    assert zero.as_tuple() == (0, 0, 0, 0, 0)
+    for fam in (nat.F32_SIMT, nat.TF32_TC, nat.BF16_TC):
+        assert lib.kp_config_valid(fam, zero) == nat.KP_ERR_INVALID_CONFIG
+    with pytest.raises(ValueError):
+        nat.to_kp_config("fast")
