@@ -380,6 +380,7 @@ kp_status kp_select_ex(kp_family family, int32_t trans_a, int32_t trans_b, int64
             best_d = 1e30;
             continue;
         }
+        if (e.batch == batch) { best = &e; break; }  // exact (always so for batch 1)
         const double d = std::fabs(std::log(double(e.batch)) - std::log(double(batch)));
         if (!best || d < best_d) { best = &e; best_d = d; }
     }
