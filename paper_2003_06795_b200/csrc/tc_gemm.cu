@@ -379,28 +379,6 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     // let the split-K reduce kernel's launch start now; its griddepcontrol.wait
     // still waits for this whole grid to finish and flush
     if (p.splits > 1) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    // TMA loads of k-tile kt of the tile at (m0, n0) into ring slot kt_all % S
-    auto issue_stage = [&](int kt_all, int kt, int m0, int n0, int za, int zb) {
-        const int s = kt_all % S;
-        mbar_expect_tx(full_bar(s), STAGE_BYTES);
-        const uint32_t sa = base + s * STAGE_BYTES;
-        const uint32_t sb = sa + A_BYTES;
-        const int k0 = kt * BK;
-        if constexpr (!A_MN) {
-            tma_load_3d(sa, &map_a, k0, m0, za, full_bar(s));
-        } else {
-#pragma unroll
-            for (int j = 0; j < BM / MA::ATOM; ++j)
-                tma_load_3d(sa + j * BK * MA::W, &map_a, m0 + j * MA::ATOM, k0, za, full_bar(s));
-        }
-        if constexpr (!B_MN) {
-            tma_load_3d(sb, &map_b, k0, n0, zb, full_bar(s));
-        } else {
-#pragma unroll
-            for (int j = 0; j < BN / MB::ATOM; ++j)
-                tma_load_3d(sb + j * BK * MB::W, &map_b, n0 + j * MB::ATOM, k0, zb, full_bar(s));
-        }
-    };
 
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < S; ++s) {
@@ -417,21 +395,6 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         if (p.tma_store)
             asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(&map_c)) : "memory");
     }
-    // The producer fills the first ring of stages of its first unit before the
-    // CTA-wide sync (the stages' empty barriers are fresh, so nothing is
-    // waited on): the first loads' latency -- tensor-map fetch included --
-    // overlaps the TMEM allocation and the sync instead of following them.
-    int pre = 0;  // stages of the first unit issued before the sync
-    if (warp == 0 && lane == 0 && int(blockIdx.x) < units) {
-        const int u = blockIdx.x;
-        int m0, n0, bz, kb0, kb1;
-        tile_coords(u / p.splits, p, BN, m0, n0, bz);
-        split_range(u % p.splits, p.splits, p.k_tiles, kb0, kb1);
-        pre = min(S, kb1 - kb0);
-        for (int i = 0; i < pre; ++i)
-            issue_stage(i, kb0 + i, m0, n0, bz * p.a_batch, bz * p.b_batch);
-        trace(2);
-    }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
                      :: "r"(smem_u32(tmem_slot)), "r"(TMEM_COLS) : "memory");
@@ -445,17 +408,37 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
 
     if (warp == 0) {
         if (lane == 0) {  // ---- TMA producer: one ring across all of this CTA's units
-            int kt_all = pre;
+            int kt_all = 0;
             for (int u = blockIdx.x; u < units; u += gridDim.x) {
                 int m0, n0, bz, kb0, kb1;
                 tile_coords(u / p.splits, p, BN, m0, n0, bz);
                 split_range(u % p.splits, p.splits, p.k_tiles, kb0, kb1);
                 const int za = bz * p.a_batch, zb = bz * p.b_batch;
-                for (int kt = kb0 + (u == int(blockIdx.x) ? pre : 0); kt < kb1; ++kt, ++kt_all) {
+                for (int kt = kb0; kt < kb1; ++kt, ++kt_all) {
                     const int s = kt_all % S;
                     const uint32_t phase = (kt_all / S) & 1;
                     mbar_wait(empty_bar(s), phase ^ 1);
-                    issue_stage(kt_all, kt, m0, n0, za, zb);
+                    mbar_expect_tx(full_bar(s), STAGE_BYTES);
+                    const uint32_t sa = base + s * STAGE_BYTES;
+                    const uint32_t sb = sa + A_BYTES;
+                    const int k0 = kt * BK;
+                    if constexpr (!A_MN) {
+                        tma_load_3d(sa, &map_a, k0, m0, za, full_bar(s));
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < BM / MA::ATOM; ++j)
+                            tma_load_3d(sa + j * BK * MA::W, &map_a, m0 + j * MA::ATOM, k0, za,
+                                        full_bar(s));
+                    }
+                    if constexpr (!B_MN) {
+                        tma_load_3d(sb, &map_b, k0, n0, zb, full_bar(s));
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < BN / MB::ATOM; ++j)
+                            tma_load_3d(sb + j * BK * MB::W, &map_b, n0 + j * MB::ATOM, k0, zb,
+                                        full_bar(s));
+                    }
+                    if (kt_all == 0) trace(2);
                 }
             }
         }
@@ -465,7 +448,6 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             for (int u = blockIdx.x; u < units; u += gridDim.x, ++it) {
                 int kb0, kb1;
                 split_range(u % p.splits, p.splits, p.k_tiles, kb0, kb1);
-
                 const int buf = NBUF == 2 ? (it & 1) : 0;
                 const uint32_t use = NBUF == 2 ? ((it >> 1) & 1) : (it & 1);
                 mbar_wait(acc_empty(buf), use ^ 1);  // epilogue drained this buffer
