@@ -836,10 +836,18 @@ def run_gpu(args) -> int:
     # ---- rank 0: roofline evidence blocks (one GPU's worth) ---------------
     extra = {}
     if not args.no_extra:
-        extra["held_out"] = held_out_block(dev)
-        extra["large_sizes"] = large_sizes_block(dev, peaks)
-        extra["network_roofline"] = network_roofline_block(dev, peaks)
-        extra["small_m"] = small_m_block(dev, peaks)
+        # evidence blocks: a failure is recorded in the line instead of
+        # losing the headline measurement
+        for name, fn in (("held_out", lambda: held_out_block(dev)),
+                         ("large_sizes", lambda: large_sizes_block(dev, peaks)),
+                         ("network_roofline", lambda: network_roofline_block(dev, peaks)),
+                         ("small_m", lambda: small_m_block(dev, peaks))):
+            try:
+                extra[name] = fn()
+            except Exception as exc:  # noqa: BLE001
+                extra[name] = {"error": f"{type(exc).__name__}: {exc}"[:500]}
+                torch.cuda.synchronize()
+                torch.cuda.empty_cache()
 
     per_size, pct_best, dom, mean_ms = f32.report(per_size_ms)
     achieved = flops_of(SIZES[dom]) / (mean_ms[dom] * 1e-3) / 1e12

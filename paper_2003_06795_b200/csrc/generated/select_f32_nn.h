@@ -21,18 +21,46 @@ static inline select_f32_nn_config select_f32_nn(int64_t m, int64_t k, int64_t n
             return out;
         } else {
             if (n < INT64_C(144)) {
-                select_f32_nn_config out = {2u, 1u, 1u, 8u, 8u};
-                return out;
+                if (n < INT64_C(79)) {
+                    if (k < INT64_C(272)) {
+                        select_f32_nn_config out = {2u, 1u, 1u, 8u, 8u};
+                        return out;
+                    } else {
+                        select_f32_nn_config out = {4u, 2u, 2u, 8u, 8u};
+                        return out;
+                    }
+                } else {
+                    select_f32_nn_config out = {2u, 1u, 1u, 8u, 8u};
+                    return out;
+                }
             } else {
                 if (n < INT64_C(544)) {
                     if (m < INT64_C(139)) {
-                        if (n < INT64_C(227)) {
-                            select_f32_nn_config out = {2u, 1u, 1u, 8u, 8u};
-                            return out;
+                        if (k < INT64_C(992)) {
+                            if (n < INT64_C(227)) {
+                                select_f32_nn_config out = {2u, 1u, 1u, 8u, 8u};
+                                return out;
+                            } else {
+                                if (m < INT64_C(70)) {
+                                    select_f32_nn_config out = {2u, 1u, 1u, 8u, 8u};
+                                    return out;
+                                } else {
+                                    select_f32_nn_config out = {4u, 2u, 2u, 8u, 8u};
+                                    return out;
+                                }
+                            }
                         } else {
-                            if (k < INT64_C(3072)) {
-                                if (k < INT64_C(992)) {
-                                    if (m < INT64_C(70)) {
+                            select_f32_nn_config out = {4u, 2u, 2u, 8u, 8u};
+                            return out;
+                        }
+                    } else {
+                        if (n < INT64_C(444)) {
+                            if (k < INT64_C(992)) {
+                                select_f32_nn_config out = {4u, 2u, 2u, 8u, 8u};
+                                return out;
+                            } else {
+                                if (m < INT64_C(278)) {
+                                    if (k < INT64_C(1537)) {
                                         select_f32_nn_config out = {2u, 1u, 1u, 8u, 8u};
                                         return out;
                                     } else {
@@ -43,31 +71,13 @@ static inline select_f32_nn_config select_f32_nn(int64_t m, int64_t k, int64_t n
                                     select_f32_nn_config out = {4u, 2u, 2u, 8u, 8u};
                                     return out;
                                 }
-                            } else {
-                                select_f32_nn_config out = {2u, 1u, 1u, 8u, 8u};
-                                return out;
-                            }
-                        }
-                    } else {
-                        if (n < INT64_C(287)) {
-                            if (k < INT64_C(1536)) {
-                                select_f32_nn_config out = {4u, 2u, 2u, 8u, 8u};
-                                return out;
-                            } else {
-                                if (m < INT64_C(278)) {
-                                    select_f32_nn_config out = {2u, 1u, 1u, 8u, 8u};
-                                    return out;
-                                } else {
-                                    select_f32_nn_config out = {4u, 2u, 2u, 8u, 8u};
-                                    return out;
-                                }
                             }
                         } else {
                             if (m < INT64_C(278)) {
                                 select_f32_nn_config out = {4u, 2u, 2u, 8u, 8u};
                                 return out;
                             } else {
-                                select_f32_nn_config out = {4u, 4u, 2u, 8u, 8u};
+                                select_f32_nn_config out = {2u, 4u, 4u, 16u, 8u};
                                 return out;
                             }
                         }
@@ -75,13 +85,8 @@ static inline select_f32_nn_config select_f32_nn(int64_t m, int64_t k, int64_t n
                 } else {
                     if (m < INT64_C(70)) {
                         if (n < INT64_C(1132)) {
-                            if (m < INT64_C(29)) {
-                                select_f32_nn_config out = {2u, 1u, 1u, 8u, 8u};
-                                return out;
-                            } else {
-                                select_f32_nn_config out = {4u, 2u, 2u, 8u, 8u};
-                                return out;
-                            }
+                            select_f32_nn_config out = {2u, 1u, 1u, 8u, 8u};
+                            return out;
                         } else {
                             select_f32_nn_config out = {4u, 2u, 2u, 8u, 8u};
                             return out;
@@ -94,21 +99,31 @@ static inline select_f32_nn_config select_f32_nn(int64_t m, int64_t k, int64_t n
                                     return out;
                                 } else {
                                     if (k < INT64_C(124)) {
-                                        select_f32_nn_config out = {4u, 4u, 2u, 8u, 8u};
+                                        select_f32_nn_config out = {4u, 2u, 2u, 8u, 8u};
                                         return out;
                                     } else {
                                         if (k < INT64_C(287)) {
                                             select_f32_nn_config out = {2u, 4u, 4u, 16u, 8u};
                                             return out;
                                         } else {
-                                            select_f32_nn_config out = {4u, 4u, 2u, 8u, 8u};
+                                            select_f32_nn_config out = {4u, 2u, 2u, 8u, 8u};
                                             return out;
                                         }
                                     }
                                 }
                             } else {
-                                select_f32_nn_config out = {2u, 4u, 4u, 16u, 8u};
-                                return out;
+                                if (m < INT64_C(139)) {
+                                    select_f32_nn_config out = {2u, 4u, 4u, 16u, 8u};
+                                    return out;
+                                } else {
+                                    if (k < INT64_C(725)) {
+                                        select_f32_nn_config out = {2u, 4u, 4u, 16u, 8u};
+                                        return out;
+                                    } else {
+                                        select_f32_nn_config out = {8u, 8u, 4u, 16u, 8u};
+                                        return out;
+                                    }
+                                }
                             }
                         } else {
                             if (k < INT64_C(405)) {
@@ -116,8 +131,8 @@ static inline select_f32_nn_config select_f32_nn(int64_t m, int64_t k, int64_t n
                                     select_f32_nn_config out = {2u, 4u, 4u, 16u, 8u};
                                     return out;
                                 } else {
-                                    if (k < INT64_C(287)) {
-                                        select_f32_nn_config out = {4u, 4u, 4u, 16u, 8u};
+                                    if (k < INT64_C(227)) {
+                                        select_f32_nn_config out = {8u, 8u, 4u, 16u, 8u};
                                         return out;
                                     } else {
                                         select_f32_nn_config out = {2u, 4u, 4u, 16u, 8u};
@@ -125,7 +140,7 @@ static inline select_f32_nn_config select_f32_nn(int64_t m, int64_t k, int64_t n
                                     }
                                 }
                             } else {
-                                select_f32_nn_config out = {4u, 8u, 4u, 16u, 8u};
+                                select_f32_nn_config out = {8u, 8u, 4u, 16u, 8u};
                                 return out;
                             }
                         }
@@ -134,367 +149,187 @@ static inline select_f32_nn_config select_f32_nn(int64_t m, int64_t k, int64_t n
             }
         }
     } else {
-        if (m < INT64_C(4435)) {
-            if (n < INT64_C(363)) {
-                if (m < INT64_C(2218)) {
-                    if (n < INT64_C(144)) {
+        if (m < INT64_C(17740)) {
+            if (n < INT64_C(444)) {
+                if (m < INT64_C(4435)) {
+                    if (n < INT64_C(176)) {
                         if (m < INT64_C(1109)) {
-                            if (k < INT64_C(236)) {
-                                select_f32_nn_config out = {2u, 1u, 1u, 8u, 8u};
-                                return out;
+                            if (k < INT64_C(222)) {
+                                if (k < INT64_C(167)) {
+                                    select_f32_nn_config out = {4u, 2u, 2u, 8u, 8u};
+                                    return out;
+                                } else {
+                                    select_f32_nn_config out = {2u, 1u, 1u, 8u, 8u};
+                                    return out;
+                                }
                             } else {
                                 select_f32_nn_config out = {4u, 2u, 2u, 8u, 8u};
                                 return out;
                             }
                         } else {
                             if (n < INT64_C(46)) {
-                                select_f32_nn_config out = {4u, 2u, 2u, 8u, 8u};
-                                return out;
-                            } else {
-                                if (k < INT64_C(363)) {
-                                    if (k < INT64_C(222)) {
-                                        select_f32_nn_config out = {4u, 4u, 2u, 8u, 8u};
+                                if (m < INT64_C(2218)) {
+                                    select_f32_nn_config out = {4u, 2u, 2u, 8u, 8u};
+                                    return out;
+                                } else {
+                                    if (n < INT64_C(28)) {
+                                        select_f32_nn_config out = {4u, 2u, 2u, 8u, 8u};
                                         return out;
                                     } else {
                                         select_f32_nn_config out = {2u, 4u, 4u, 16u, 8u};
                                         return out;
                                     }
+                                }
+                            } else {
+                                if (m < INT64_C(2218)) {
+                                    if (k < INT64_C(444)) {
+                                        if (k < INT64_C(314)) {
+                                            select_f32_nn_config out = {2u, 4u, 4u, 16u, 8u};
+                                            return out;
+                                        } else {
+                                            select_f32_nn_config out = {4u, 2u, 2u, 8u, 8u};
+                                            return out;
+                                        }
+                                    } else {
+                                        select_f32_nn_config out = {2u, 4u, 4u, 16u, 8u};
+                                        return out;
+                                    }
                                 } else {
-                                    select_f32_nn_config out = {4u, 4u, 2u, 8u, 8u};
+                                    select_f32_nn_config out = {2u, 4u, 4u, 16u, 8u};
                                     return out;
                                 }
                             }
                         }
                     } else {
-                        if (k < INT64_C(128)) {
-                            if (m < INT64_C(1109)) {
-                                select_f32_nn_config out = {2u, 4u, 4u, 16u, 8u};
-                                return out;
-                            } else {
-                                select_f32_nn_config out = {4u, 4u, 4u, 16u, 8u};
-                                return out;
-                            }
+                        if (m < INT64_C(1109)) {
+                            select_f32_nn_config out = {2u, 4u, 4u, 16u, 8u};
+                            return out;
                         } else {
-                            if (k < INT64_C(544)) {
-                                if (m < INT64_C(1109)) {
-                                    select_f32_nn_config out = {4u, 4u, 2u, 8u, 8u};
+                            if (m < INT64_C(2218)) {
+                                if (k < INT64_C(46)) {
+                                    select_f32_nn_config out = {8u, 8u, 4u, 16u, 8u};
                                     return out;
                                 } else {
-                                    select_f32_nn_config out = {4u, 8u, 4u, 16u, 8u};
-                                    return out;
+                                    if (k < INT64_C(725)) {
+                                        select_f32_nn_config out = {2u, 4u, 4u, 16u, 8u};
+                                        return out;
+                                    } else {
+                                        if (k < INT64_C(1537)) {
+                                            select_f32_nn_config out = {8u, 8u, 4u, 16u, 8u};
+                                            return out;
+                                        } else {
+                                            select_f32_nn_config out = {2u, 4u, 4u, 16u, 8u};
+                                            return out;
+                                        }
+                                    }
                                 }
                             } else {
-                                select_f32_nn_config out = {4u, 4u, 2u, 8u, 8u};
+                                select_f32_nn_config out = {2u, 4u, 4u, 16u, 8u};
                                 return out;
                             }
                         }
                     }
                 } else {
-                    if (n < INT64_C(46)) {
-                        select_f32_nn_config out = {4u, 4u, 2u, 8u, 8u};
-                        return out;
-                    } else {
-                        if (n < INT64_C(111)) {
-                            if (k < INT64_C(314)) {
-                                if (k < INT64_C(222)) {
+                    if (k < INT64_C(168)) {
+                        if (n < INT64_C(222)) {
+                            if (n < INT64_C(28)) {
+                                if (m < INT64_C(8870)) {
                                     select_f32_nn_config out = {2u, 4u, 4u, 16u, 8u};
                                     return out;
                                 } else {
-                                    select_f32_nn_config out = {4u, 4u, 4u, 16u, 8u};
-                                    return out;
+                                    if (k < INT64_C(56)) {
+                                        select_f32_nn_config out = {2u, 4u, 4u, 16u, 8u};
+                                        return out;
+                                    } else {
+                                        if (k < INT64_C(118)) {
+                                            select_f32_nn_config out = {8u, 8u, 4u, 16u, 8u};
+                                            return out;
+                                        } else {
+                                            select_f32_nn_config out = {2u, 4u, 4u, 16u, 8u};
+                                            return out;
+                                        }
+                                    }
                                 }
                             } else {
                                 select_f32_nn_config out = {2u, 4u, 4u, 16u, 8u};
                                 return out;
                             }
                         } else {
-                            if (n < INT64_C(222)) {
-                                if (k < INT64_C(28)) {
-                                    select_f32_nn_config out = {4u, 4u, 4u, 16u, 8u};
-                                    return out;
-                                } else {
-                                    select_f32_nn_config out = {4u, 4u, 2u, 8u, 8u};
-                                    return out;
-                                }
-                            } else {
-                                if (k < INT64_C(725)) {
-                                    select_f32_nn_config out = {4u, 4u, 4u, 16u, 8u};
-                                    return out;
-                                } else {
-                                    if (k < INT64_C(1087)) {
+                            select_f32_nn_config out = {8u, 8u, 4u, 16u, 8u};
+                            return out;
+                        }
+                    } else {
+                        if (n < INT64_C(182)) {
+                            if (m < INT64_C(8870)) {
+                                if (n < INT64_C(91)) {
+                                    if (k < INT64_C(222)) {
                                         select_f32_nn_config out = {2u, 4u, 4u, 16u, 8u};
                                         return out;
                                     } else {
-                                        select_f32_nn_config out = {4u, 4u, 4u, 16u, 8u};
+                                        select_f32_nn_config out = {8u, 8u, 4u, 16u, 8u};
                                         return out;
                                     }
+                                } else {
+                                    select_f32_nn_config out = {2u, 4u, 4u, 16u, 8u};
+                                    return out;
+                                }
+                            } else {
+                                if (n < INT64_C(91)) {
+                                    if (k < INT64_C(222)) {
+                                        select_f32_nn_config out = {8u, 8u, 4u, 16u, 8u};
+                                        return out;
+                                    } else {
+                                        select_f32_nn_config out = {2u, 4u, 4u, 16u, 8u};
+                                        return out;
+                                    }
+                                } else {
+                                    select_f32_nn_config out = {8u, 8u, 4u, 16u, 8u};
+                                    return out;
                                 }
                             }
+                        } else {
+                            select_f32_nn_config out = {8u, 8u, 4u, 16u, 8u};
+                            return out;
                         }
                     }
                 }
             } else {
                 if (m < INT64_C(1792)) {
-                    if (n < INT64_C(544)) {
-                        if (m < INT64_C(1109)) {
-                            if (k < INT64_C(725)) {
-                                if (m < INT64_C(634)) {
+                    if (k < INT64_C(111)) {
+                        select_f32_nn_config out = {8u, 8u, 4u, 16u, 8u};
+                        return out;
+                    } else {
+                        if (k < INT64_C(1449)) {
+                            if (n < INT64_C(992)) {
+                                select_f32_nn_config out = {2u, 4u, 4u, 16u, 8u};
+                                return out;
+                            } else {
+                                if (k < INT64_C(405)) {
+                                    select_f32_nn_config out = {8u, 8u, 4u, 16u, 8u};
+                                    return out;
+                                } else {
                                     select_f32_nn_config out = {2u, 4u, 4u, 16u, 8u};
                                     return out;
-                                } else {
-                                    if (k < INT64_C(182)) {
-                                        select_f32_nn_config out = {2u, 4u, 4u, 16u, 8u};
-                                        return out;
-                                    } else {
-                                        select_f32_nn_config out = {4u, 8u, 4u, 16u, 8u};
-                                        return out;
-                                    }
-                                }
-                            } else {
-                                select_f32_nn_config out = {4u, 4u, 2u, 8u, 8u};
-                                return out;
-                            }
-                        } else {
-                            select_f32_nn_config out = {4u, 4u, 4u, 16u, 8u};
-                            return out;
-                        }
-                    } else {
-                        if (m < INT64_C(896)) {
-                            if (k < INT64_C(124)) {
-                                select_f32_nn_config out = {4u, 8u, 4u, 16u, 8u};
-                                return out;
-                            } else {
-                                if (k < INT64_C(287)) {
-                                    select_f32_nn_config out = {4u, 4u, 4u, 16u, 8u};
-                                    return out;
-                                } else {
-                                    if (k < INT64_C(405)) {
-                                        select_f32_nn_config out = {4u, 8u, 4u, 16u, 8u};
-                                        return out;
-                                    } else {
-                                        select_f32_nn_config out = {4u, 4u, 4u, 16u, 8u};
-                                        return out;
-                                    }
                                 }
                             }
                         } else {
-                            select_f32_nn_config out = {4u, 8u, 4u, 16u, 8u};
-                            return out;
+                            if (m < INT64_C(1109)) {
+                                select_f32_nn_config out = {8u, 8u, 4u, 16u, 8u};
+                                return out;
+                            } else {
+                                select_f32_nn_config out = {2u, 4u, 4u, 16u, 8u};
+                                return out;
+                            }
                         }
                     }
                 } else {
-                    if (n < INT64_C(768)) {
-                        select_f32_nn_config out = {4u, 8u, 4u, 16u, 8u};
-                        return out;
-                    } else {
-                        if (m < INT64_C(2535)) {
-                            select_f32_nn_config out = {4u, 8u, 4u, 16u, 8u};
-                            return out;
-                        } else {
-                            select_f32_nn_config out = {4u, 8u, 8u, 16u, 8u};
-                            return out;
-                        }
-                    }
+                    select_f32_nn_config out = {8u, 8u, 4u, 16u, 8u};
+                    return out;
                 }
             }
         } else {
-            if (n < INT64_C(28)) {
-                if (m < INT64_C(8870)) {
-                    select_f32_nn_config out = {2u, 4u, 4u, 16u, 8u};
-                    return out;
-                } else {
-                    if (k < INT64_C(118)) {
-                        select_f32_nn_config out = {4u, 2u, 8u, 128u, 1u};
-                        return out;
-                    } else {
-                        if (m < INT64_C(35480)) {
-                            select_f32_nn_config out = {4u, 2u, 8u, 128u, 1u};
-                            return out;
-                        } else {
-                            select_f32_nn_config out = {4u, 8u, 4u, 16u, 8u};
-                            return out;
-                        }
-                    }
-                }
-            } else {
-                if (m < INT64_C(70960)) {
-                    if (k < INT64_C(815)) {
-                        if (m < INT64_C(17740)) {
-                            if (n < INT64_C(167)) {
-                                if (k < INT64_C(363)) {
-                                    if (m < INT64_C(8870)) {
-                                        if (k < INT64_C(167)) {
-                                            if (k < INT64_C(59)) {
-                                                select_f32_nn_config out = {2u, 4u, 4u, 16u, 8u};
-                                                return out;
-                                            } else {
-                                                select_f32_nn_config out = {4u, 4u, 4u, 16u, 8u};
-                                                return out;
-                                            }
-                                        } else {
-                                            select_f32_nn_config out = {2u, 4u, 4u, 16u, 8u};
-                                            return out;
-                                        }
-                                    } else {
-                                        if (k < INT64_C(96)) {
-                                            if (k < INT64_C(20)) {
-                                                select_f32_nn_config out = {4u, 4u, 4u, 16u, 8u};
-                                                return out;
-                                            } else {
-                                                if (n < INT64_C(46)) {
-                                                    select_f32_nn_config out = {4u, 4u, 4u, 16u, 8u};
-                                                    return out;
-                                                } else {
-                                                    select_f32_nn_config out = {4u, 8u, 4u, 16u, 8u};
-                                                    return out;
-                                                }
-                                            }
-                                        } else {
-                                            if (k < INT64_C(168)) {
-                                                select_f32_nn_config out = {2u, 4u, 4u, 16u, 8u};
-                                                return out;
-                                            } else {
-                                                if (k < INT64_C(222)) {
-                                                    select_f32_nn_config out = {4u, 8u, 4u, 16u, 8u};
-                                                    return out;
-                                                } else {
-                                                    select_f32_nn_config out = {4u, 4u, 4u, 16u, 8u};
-                                                    return out;
-                                                }
-                                            }
-                                        }
-                                    }
-                                } else {
-                                    if (m < INT64_C(8870)) {
-                                        if (k < INT64_C(544)) {
-                                            select_f32_nn_config out = {4u, 4u, 4u, 16u, 8u};
-                                            return out;
-                                        } else {
-                                            select_f32_nn_config out = {4u, 8u, 4u, 16u, 8u};
-                                            return out;
-                                        }
-                                    } else {
-                                        select_f32_nn_config out = {4u, 8u, 4u, 16u, 8u};
-                                        return out;
-                                    }
-                                }
-                            } else {
-                                if (k < INT64_C(182)) {
-                                    select_f32_nn_config out = {4u, 8u, 4u, 16u, 8u};
-                                    return out;
-                                } else {
-                                    if (m < INT64_C(8870)) {
-                                        select_f32_nn_config out = {4u, 8u, 8u, 16u, 8u};
-                                        return out;
-                                    } else {
-                                        select_f32_nn_config out = {4u, 8u, 4u, 16u, 8u};
-                                        return out;
-                                    }
-                                }
-                            }
-                        } else {
-                            if (k < INT64_C(26)) {
-                                select_f32_nn_config out = {4u, 8u, 4u, 16u, 8u};
-                                return out;
-                            } else {
-                                if (k < INT64_C(42)) {
-                                    if (n < INT64_C(46)) {
-                                        select_f32_nn_config out = {4u, 8u, 4u, 16u, 8u};
-                                        return out;
-                                    } else {
-                                        select_f32_nn_config out = {4u, 8u, 8u, 16u, 8u};
-                                        return out;
-                                    }
-                                } else {
-                                    if (k < INT64_C(97)) {
-                                        select_f32_nn_config out = {4u, 8u, 4u, 16u, 8u};
-                                        return out;
-                                    } else {
-                                        if (m < INT64_C(35480)) {
-                                            if (n < INT64_C(91)) {
-                                                select_f32_nn_config out = {4u, 8u, 4u, 16u, 8u};
-                                                return out;
-                                            } else {
-                                                select_f32_nn_config out = {4u, 8u, 8u, 16u, 8u};
-                                                return out;
-                                            }
-                                        } else {
-                                            if (k < INT64_C(291)) {
-                                                select_f32_nn_config out = {4u, 8u, 8u, 16u, 8u};
-                                                return out;
-                                            } else {
-                                                select_f32_nn_config out = {4u, 8u, 4u, 16u, 8u};
-                                                return out;
-                                            }
-                                        }
-                                    }
-                                }
-                            }
-                        }
-                    } else {
-                        if (n < INT64_C(182)) {
-                            if (m < INT64_C(8870)) {
-                                select_f32_nn_config out = {4u, 4u, 4u, 16u, 8u};
-                                return out;
-                            } else {
-                                if (m < INT64_C(17740)) {
-                                    select_f32_nn_config out = {4u, 8u, 4u, 16u, 8u};
-                                    return out;
-                                } else {
-                                    if (m < INT64_C(35480)) {
-                                        select_f32_nn_config out = {4u, 8u, 8u, 16u, 8u};
-                                        return out;
-                                    } else {
-                                        select_f32_nn_config out = {4u, 8u, 4u, 16u, 8u};
-                                        return out;
-                                    }
-                                }
-                            }
-                        } else {
-                            if (m < INT64_C(25088)) {
-                                if (k < INT64_C(6144)) {
-                                    select_f32_nn_config out = {4u, 8u, 4u, 16u, 8u};
-                                    return out;
-                                } else {
-                                    select_f32_nn_config out = {4u, 8u, 8u, 16u, 8u};
-                                    return out;
-                                }
-                            } else {
-                                select_f32_nn_config out = {4u, 8u, 8u, 16u, 8u};
-                                return out;
-                            }
-                        }
-                    }
-                } else {
-                    if (k < INT64_C(21)) {
-                        select_f32_nn_config out = {4u, 8u, 4u, 16u, 8u};
-                        return out;
-                    } else {
-                        if (n < INT64_C(46)) {
-                            select_f32_nn_config out = {4u, 8u, 4u, 16u, 8u};
-                            return out;
-                        } else {
-                            if (m < INT64_C(141920)) {
-                                if (k < INT64_C(291)) {
-                                    select_f32_nn_config out = {4u, 8u, 8u, 16u, 8u};
-                                    return out;
-                                } else {
-                                    if (n < INT64_C(91)) {
-                                        select_f32_nn_config out = {4u, 8u, 4u, 16u, 8u};
-                                        return out;
-                                    } else {
-                                        select_f32_nn_config out = {4u, 8u, 8u, 16u, 8u};
-                                        return out;
-                                    }
-                                }
-                            } else {
-                                select_f32_nn_config out = {4u, 8u, 8u, 16u, 8u};
-                                return out;
-                            }
-                        }
-                    }
-                }
-            }
+            select_f32_nn_config out = {8u, 8u, 4u, 16u, 8u};
+            return out;
         }
     }
 }
