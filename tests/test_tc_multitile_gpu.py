@@ -123,7 +123,8 @@ def test_persistent_batched_multitile(family):
 
 
 # the configs tools/large_sizes.py reports at 8192^3 (the large-size table)
-LARGE_8192 = [(4, 1, 8, 16, 16), (8, 1, 8, 16, 16), (4, 2, 8, 16, 16), (4, 1, 8, 8, 8)]
+LARGE_8192 = [(4, 1, 8, 16, 16), (8, 1, 8, 16, 16), (4, 2, 8, 16, 16), (8, 2, 8, 16, 16),
+              (4, 1, 8, 8, 8)]
 
 
 @pytest.mark.parametrize("family", ["bf16", "tf32"])
