@@ -70,10 +70,15 @@ def main() -> int:
                 dt = torch.bfloat16 if fam == "bf16" else torch.float32
                 x, w = x32.to(dt), w32.to(dt)
                 kk = cin * k * k
-                if fam != "f32" and (kk * (2 if fam == "bf16" else 4)) % 16:
-                    row[fam] = {"skipped": "K pitch not 16-byte aligned (TMA)"}
-                    continue
-                ws = torch.empty(args.batch * ho * ho * kk, dtype=dt, device="cuda")
+                # the workspace kp_conv2d_auto needs (16-byte K pitch for the
+                # tensor-core families: conv1_1 / conv1 run since round 2)
+                import ctypes
+                from paper_2003_06795_b200 import _native as nat
+                need = ctypes.c_int64()
+                d = conv._desc(x, w, st, pad)
+                nat.check(nat.lib().kp_conv_workspace_elems(nat.family_id(fam), ctypes.byref(d),
+                                                            ctypes.byref(need)))
+                ws = torch.empty(need.value, dtype=dt, device="cuda")
                 ms = time_ms(lambda: conv.conv2d(x, w, st, pad, family=fam, nhwc=True,
                                                  workspace=ws))
                 im_ms = time_ms(lambda: conv.im2col(x, k, k, st, pad, family=fam))
