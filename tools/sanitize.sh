@@ -32,3 +32,20 @@ for tool in memcheck racecheck; do
     run --tool $tool python tools/run_config.py --family $fam --trans tt --cfg 4,2,8,16,16 --mkn 4096,96,4352 --iters 1 --no-time
   done
 done
+# small-M path (K6): B normal / transposed, vector and scalar (unaligned)
+# kernels, split-K last-CTA finish, fp32 and bf16 (round 2)
+for tool in memcheck racecheck; do
+  for fam in f32 bf16; do
+    for t in nn nt tn tt; do
+      run --tool $tool python tools/run_config.py --family $fam --trans $t --cfg 0,0,0,0,0 --mkn 5,3000,520 --iters 2 --no-time
+    done
+    run --tool $tool python tools/run_config.py --family $fam --trans nn --cfg 0,0,0,0,0 --mkn 16,4096,1000 --iters 2 --no-time
+    run --tool $tool python tools/run_config.py --family $fam --trans nt --cfg 0,0,0,0,0 --mkn 1,25088,512 --iters 2 --no-time
+    run --tool $tool python tools/run_config.py --family $fam --trans nn --cfg 0,0,0,0,0 --mkn 3,777,333 --iters 2 --no-time
+  done
+done
+# tcgen05 TMA-store epilogue and split-K partials through TMA (round 2)
+for tool in memcheck racecheck; do
+  run --tool $tool python tools/run_config.py --family bf16 --trans nn --cfg 1,1,4,8,8 --mkn 1000,520,1000 --iters 2 --no-time
+  run --tool $tool python tools/run_config.py --family tf32 --trans tt --cfg 2,1,4,8,8 --mkn 392,4608,512 --iters 2 --no-time
+done
