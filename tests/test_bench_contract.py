@@ -114,3 +114,27 @@ def test_pinned_pipeline_row_blocks(m, k, want):
     assert blocks[0][0] == 0 and blocks[-1][1] == m
     assert all(a[1] == b[0] for a, b in zip(blocks, blocks[1:]))
     assert len(blocks) == want
+
+
+def test_cpu_port_baseline_runs_on_cpu(monkeypatch):
+    """The CPU arm times the oracle restatement (kind "port") at all host
+    threads and at one thread, with numpy/OpenBLAS only as context; on a
+    tiny square set it runs here."""
+    import bench
+    monkeypatch.setattr(bench, "SIZES", (16, 32))
+    line = bench.cpu_baseline(0.05)
+    assert line["kind"] == "port" and line["unit"] == "TFLOP/s"
+    assert line["value"] > 0 and line["one_core"]["value"] > 0 and line["one_core"]["cores"] == 1
+    assert line["cpu_blas"]["value"] > 0
+    assert "oracle/gemm_ref.c" in line["sample"]
+
+
+def test_reference_arm_runs_on_cpu(monkeypatch, capsys):
+    import bench
+    monkeypatch.setattr(bench, "SIZES", (16, 32))
+    monkeypatch.delenv("RANK", raising=False)
+    args = bench.parse_args(["--impl", "reference", "--steps", "2", "--warmup", "3"])
+    assert bench.run_reference(args) == 0
+    line = json.loads(capsys.readouterr().out.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["config"] == bench.bench_config(1)
+    assert line["e2e"]["value"] == line["value"] and line["cpu_baseline"]["kind"] == "port"
