@@ -15,115 +15,148 @@ static inline select_tf32_tn_config select_tf32_tn(int64_t m, int64_t k, int64_t
     (void)m;
     (void)k;
     (void)n;
-    if (k < INT64_C(1087)) {
-        if (m < INT64_C(70960)) {
-            if (n < INT64_C(351)) {
-                if (m < INT64_C(8870)) {
-                    if (k < INT64_C(444)) {
-                        if (k < INT64_C(79)) {
-                            if (m < INT64_C(2218)) {
-                                if (m < INT64_C(224)) {
+    if (k < INT64_C(992)) {
+        if (m < INT64_C(35480)) {
+            if (m < INT64_C(448)) {
+                if (k < INT64_C(351)) {
+                    if (k < INT64_C(79)) {
+                        if (m < INT64_C(113)) {
+                            select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
+                            return out;
+                        } else {
+                            select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
+                            return out;
+                        }
+                    } else {
+                        select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
+                        return out;
+                    }
+                } else {
+                    if (n < INT64_C(79)) {
+                        select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
+                        return out;
+                    } else {
+                        if (n < INT64_C(287)) {
+                            if (k < INT64_C(444)) {
+                                if (m < INT64_C(278)) {
                                     select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
                                     return out;
                                 } else {
-                                    select_tf32_tn_config out = {2u, 1u, 1u, 16u, 16u};
+                                    select_tf32_tn_config out = {8u, 1u, 2u, 8u, 8u};
                                     return out;
                                 }
                             } else {
-                                if (k < INT64_C(28)) {
-                                    if (m < INT64_C(4435)) {
-                                        select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
+                                select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
+                                return out;
+                            }
+                        } else {
+                            if (m < INT64_C(278)) {
+                                if (m < INT64_C(70)) {
+                                    if (k < INT64_C(702)) {
+                                        select_tf32_tn_config out = {1u, 1u, 4u, 16u, 16u};
                                         return out;
                                     } else {
                                         select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
                                         return out;
                                     }
                                 } else {
-                                    if (m < INT64_C(4435)) {
-                                        if (k < INT64_C(46)) {
-                                            select_tf32_tn_config out = {1u, 1u, 4u, 16u, 16u};
-                                            return out;
-                                        } else {
-                                            select_tf32_tn_config out = {8u, 1u, 8u, 8u, 8u};
-                                            return out;
-                                        }
+                                    if (m < INT64_C(139)) {
+                                        select_tf32_tn_config out = {8u, 1u, 2u, 8u, 8u};
+                                        return out;
                                     } else {
-                                        if (k < INT64_C(46)) {
-                                            select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
+                                        if (k < INT64_C(702)) {
+                                            select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
                                             return out;
                                         } else {
-                                            select_tf32_tn_config out = {1u, 1u, 4u, 16u, 16u};
+                                            select_tf32_tn_config out = {8u, 1u, 2u, 8u, 8u};
                                             return out;
                                         }
                                     }
                                 }
+                            } else {
+                                if (k < INT64_C(702)) {
+                                    select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
+                                    return out;
+                                } else {
+                                    select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
+                                    return out;
+                                }
                             }
+                        }
+                    }
+                }
+            } else {
+                if (n < INT64_C(136)) {
+                    if (k < INT64_C(30)) {
+                        if (m < INT64_C(17740)) {
+                            select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
+                            return out;
                         } else {
-                            if (m < INT64_C(555)) {
-                                select_tf32_tn_config out = {2u, 1u, 1u, 16u, 16u};
+                            if (k < INT64_C(21)) {
+                                select_tf32_tn_config out = {4u, 2u, 8u, 16u, 16u};
                                 return out;
                             } else {
-                                if (n < INT64_C(46)) {
+                                select_tf32_tn_config out = {1u, 1u, 4u, 8u, 8u};
+                                return out;
+                            }
+                        }
+                    } else {
+                        if (n < INT64_C(46)) {
+                            if (k < INT64_C(167)) {
+                                if (m < INT64_C(4435)) {
+                                    select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
+                                    return out;
+                                } else {
                                     if (k < INT64_C(118)) {
-                                        if (m < INT64_C(4435)) {
-                                            select_tf32_tn_config out = {2u, 1u, 1u, 16u, 16u};
-                                            return out;
+                                        if (k < INT64_C(56)) {
+                                            if (m < INT64_C(17740)) {
+                                                select_tf32_tn_config out = {1u, 1u, 4u, 8u, 8u};
+                                                return out;
+                                            } else {
+                                                select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
+                                                return out;
+                                            }
                                         } else {
                                             select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
                                             return out;
                                         }
                                     } else {
-                                        if (m < INT64_C(2218)) {
-                                            if (m < INT64_C(1109)) {
-                                                select_tf32_tn_config out = {2u, 1u, 1u, 16u, 16u};
+                                        if (m < INT64_C(8870)) {
+                                            if (n < INT64_C(28)) {
+                                                select_tf32_tn_config out = {4u, 2u, 8u, 16u, 16u};
                                                 return out;
                                             } else {
-                                                if (k < INT64_C(167)) {
-                                                    select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
-                                                    return out;
-                                                } else {
-                                                    select_tf32_tn_config out = {2u, 1u, 1u, 16u, 16u};
-                                                    return out;
-                                                }
+                                                select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
+                                                return out;
                                             }
                                         } else {
-                                            select_tf32_tn_config out = {2u, 1u, 1u, 16u, 16u};
-                                            return out;
-                                        }
-                                    }
-                                } else {
-                                    if (m < INT64_C(2218)) {
-                                        if (n < INT64_C(79)) {
-                                            if (m < INT64_C(1109)) {
-                                                if (k < INT64_C(272)) {
-                                                    select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
+                                            if (m < INT64_C(17740)) {
+                                                if (n < INT64_C(28)) {
+                                                    select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
                                                     return out;
                                                 } else {
-                                                    select_tf32_tn_config out = {2u, 1u, 1u, 16u, 16u};
+                                                    select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
                                                     return out;
                                                 }
                                             } else {
                                                 select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
                                                 return out;
                                             }
-                                        } else {
-                                            select_tf32_tn_config out = {2u, 1u, 1u, 16u, 16u};
-                                            return out;
                                         }
+                                    }
+                                }
+                            } else {
+                                if (m < INT64_C(2218)) {
+                                    select_tf32_tn_config out = {1u, 1u, 4u, 8u, 8u};
+                                    return out;
+                                } else {
+                                    if (m < INT64_C(4435)) {
+                                        select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
+                                        return out;
                                     } else {
-                                        if (n < INT64_C(79)) {
-                                            if (m < INT64_C(4435)) {
-                                                if (k < INT64_C(272)) {
-                                                    select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
-                                                    return out;
-                                                } else {
-                                                    select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
-                                                    return out;
-                                                }
-                                            } else {
-                                                select_tf32_tn_config out = {2u, 1u, 1u, 16u, 16u};
-                                                return out;
-                                            }
+                                        if (m < INT64_C(8870)) {
+                                            select_tf32_tn_config out = {1u, 1u, 4u, 8u, 8u};
+                                            return out;
                                         } else {
                                             select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
                                             return out;
@@ -131,61 +164,59 @@ static inline select_tf32_tn_config select_tf32_tn(int64_t m, int64_t k, int64_t
                                     }
                                 }
                             }
-                        }
-                    } else {
-                        if (m < INT64_C(278)) {
-                            if (n < INT64_C(203)) {
-                                if (k < INT64_C(744)) {
-                                    select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
-                                    return out;
-                                } else {
-                                    if (m < INT64_C(70)) {
-                                        select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
-                                        return out;
-                                    } else {
-                                        select_tf32_tn_config out = {2u, 1u, 1u, 16u, 16u};
-                                        return out;
-                                    }
-                                }
-                            } else {
-                                if (m < INT64_C(139)) {
-                                    select_tf32_tn_config out = {2u, 1u, 1u, 16u, 16u};
-                                    return out;
-                                } else {
-                                    if (n < INT64_C(287)) {
-                                        select_tf32_tn_config out = {2u, 1u, 1u, 16u, 16u};
-                                        return out;
-                                    } else {
-                                        select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
-                                        return out;
-                                    }
-                                }
-                            }
                         } else {
-                            if (n < INT64_C(287)) {
-                                if (k < INT64_C(992)) {
-                                    if (n < INT64_C(79)) {
-                                        select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
-                                        return out;
-                                    } else {
-                                        if (k < INT64_C(744)) {
-                                            if (k < INT64_C(544)) {
-                                                if (m < INT64_C(2218)) {
-                                                    if (n < INT64_C(182)) {
-                                                        if (m < INT64_C(1109)) {
-                                                            select_tf32_tn_config out = {1u, 1u, 4u, 16u, 16u};
+                            if (m < INT64_C(17740)) {
+                                if (k < INT64_C(544)) {
+                                    if (m < INT64_C(8870)) {
+                                        if (k < INT64_C(222)) {
+                                            if (m < INT64_C(1568)) {
+                                                select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
+                                                return out;
+                                            } else {
+                                                if (m < INT64_C(4435)) {
+                                                    if (k < INT64_C(111)) {
+                                                        select_tf32_tn_config out = {8u, 1u, 2u, 8u, 8u};
+                                                        return out;
+                                                    } else {
+                                                        select_tf32_tn_config out = {1u, 1u, 4u, 8u, 8u};
+                                                        return out;
+                                                    }
+                                                } else {
+                                                    select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
+                                                    return out;
+                                                }
+                                            }
+                                        } else {
+                                            if (n < INT64_C(79)) {
+                                                if (m < INT64_C(1109)) {
+                                                    select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
+                                                    return out;
+                                                } else {
+                                                    if (m < INT64_C(2218)) {
+                                                        select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
+                                                        return out;
+                                                    } else {
+                                                        if (m < INT64_C(4435)) {
+                                                            select_tf32_tn_config out = {8u, 1u, 2u, 8u, 8u};
                                                             return out;
                                                         } else {
-                                                            select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
+                                                            select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
                                                             return out;
                                                         }
+                                                    }
+                                                }
+                                            } else {
+                                                if (m < INT64_C(4435)) {
+                                                    if (k < INT64_C(444)) {
+                                                        select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
+                                                        return out;
                                                     } else {
-                                                        if (m < INT64_C(555)) {
+                                                        if (m < INT64_C(1109)) {
                                                             select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
                                                             return out;
                                                         } else {
-                                                            if (m < INT64_C(1109)) {
-                                                                select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
+                                                            if (m < INT64_C(2218)) {
+                                                                select_tf32_tn_config out = {1u, 1u, 4u, 8u, 8u};
                                                                 return out;
                                                             } else {
                                                                 select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
@@ -194,30 +225,22 @@ static inline select_tf32_tn_config select_tf32_tn(int64_t m, int64_t k, int64_t
                                                         }
                                                     }
                                                 } else {
-                                                    select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
-                                                    return out;
-                                                }
-                                            } else {
-                                                if (m < INT64_C(1109)) {
-                                                    if (n < INT64_C(124)) {
+                                                    if (k < INT64_C(363)) {
+                                                        select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
+                                                        return out;
+                                                    } else {
                                                         select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
-                                                        return out;
-                                                    } else {
-                                                        select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
-                                                        return out;
-                                                    }
-                                                } else {
-                                                    if (m < INT64_C(2218)) {
-                                                        select_tf32_tn_config out = {2u, 1u, 1u, 16u, 16u};
-                                                        return out;
-                                                    } else {
-                                                        select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
                                                         return out;
                                                     }
                                                 }
                                             }
-                                        } else {
+                                        }
+                                    } else {
+                                        if (n < INT64_C(91)) {
                                             select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
+                                            return out;
+                                        } else {
+                                            select_tf32_tn_config out = {1u, 1u, 4u, 16u, 16u};
                                             return out;
                                         }
                                     }
@@ -226,208 +249,21 @@ static inline select_tf32_tn_config select_tf32_tn(int64_t m, int64_t k, int64_t
                                         select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
                                         return out;
                                     } else {
-                                        select_tf32_tn_config out = {1u, 1u, 4u, 16u, 16u};
-                                        return out;
-                                    }
-                                }
-                            } else {
-                                select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
-                                return out;
-                            }
-                        }
-                    }
-                } else {
-                    if (n < INT64_C(28)) {
-                        if (m < INT64_C(17740)) {
-                            if (k < INT64_C(56)) {
-                                select_tf32_tn_config out = {8u, 2u, 4u, 16u, 16u};
-                                return out;
-                            } else {
-                                if (k < INT64_C(118)) {
-                                    select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
-                                    return out;
-                                } else {
-                                    select_tf32_tn_config out = {2u, 1u, 1u, 16u, 16u};
-                                    return out;
-                                }
-                            }
-                        } else {
-                            if (m < INT64_C(35480)) {
-                                select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
-                                return out;
-                            } else {
-                                if (k < INT64_C(118)) {
-                                    select_tf32_tn_config out = {2u, 1u, 1u, 16u, 16u};
-                                    return out;
-                                } else {
-                                    select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
-                                    return out;
-                                }
-                            }
-                        }
-                    } else {
-                        if (m < INT64_C(17740)) {
-                            if (n < INT64_C(91)) {
-                                if (n < INT64_C(46)) {
-                                    if (k < INT64_C(63)) {
-                                        select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
-                                        return out;
-                                    } else {
-                                        if (k < INT64_C(167)) {
-                                            select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
-                                            return out;
-                                        } else {
-                                            select_tf32_tn_config out = {2u, 1u, 1u, 16u, 16u};
-                                            return out;
-                                        }
-                                    }
-                                } else {
-                                    select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
-                                    return out;
-                                }
-                            } else {
-                                if (n < INT64_C(222)) {
-                                    if (k < INT64_C(363)) {
-                                        if (k < INT64_C(91)) {
-                                            select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
-                                            return out;
-                                        } else {
-                                            select_tf32_tn_config out = {8u, 2u, 4u, 16u, 16u};
-                                            return out;
-                                        }
-                                    } else {
-                                        select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
-                                        return out;
-                                    }
-                                } else {
-                                    select_tf32_tn_config out = {8u, 1u, 8u, 8u, 8u};
-                                    return out;
-                                }
-                            }
-                        } else {
-                            if (k < INT64_C(97)) {
-                                if (k < INT64_C(42)) {
-                                    if (m < INT64_C(35480)) {
-                                        if (k < INT64_C(20)) {
-                                            select_tf32_tn_config out = {1u, 1u, 4u, 16u, 16u};
-                                            return out;
-                                        } else {
-                                            select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
-                                            return out;
-                                        }
-                                    } else {
-                                        if (k < INT64_C(26)) {
-                                            select_tf32_tn_config out = {4u, 2u, 8u, 16u, 16u};
-                                            return out;
-                                        } else {
-                                            select_tf32_tn_config out = {1u, 1u, 4u, 16u, 16u};
-                                            return out;
-                                        }
-                                    }
-                                } else {
-                                    if (m < INT64_C(35480)) {
-                                        select_tf32_tn_config out = {8u, 2u, 4u, 16u, 16u};
-                                        return out;
-                                    } else {
-                                        if (n < INT64_C(128)) {
-                                            select_tf32_tn_config out = {8u, 2u, 4u, 16u, 16u};
-                                            return out;
-                                        } else {
-                                            select_tf32_tn_config out = {2u, 1u, 8u, 16u, 16u};
-                                            return out;
-                                        }
-                                    }
-                                }
-                            } else {
-                                select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
-                                return out;
-                            }
-                        }
-                    }
-                }
-            } else {
-                if (m < INT64_C(4435)) {
-                    if (m < INT64_C(2218)) {
-                        if (k < INT64_C(287)) {
-                            if (k < INT64_C(111)) {
-                                if (m < INT64_C(784)) {
-                                    if (k < INT64_C(79)) {
-                                        select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
-                                        return out;
-                                    } else {
-                                        select_tf32_tn_config out = {2u, 1u, 1u, 16u, 16u};
-                                        return out;
-                                    }
-                                } else {
-                                    select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
-                                    return out;
-                                }
-                            } else {
-                                if (n < INT64_C(992)) {
-                                    if (k < INT64_C(203)) {
-                                        if (m < INT64_C(139)) {
-                                            select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
-                                            return out;
-                                        } else {
-                                            if (m < INT64_C(278)) {
-                                                select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
+                                        if (m < INT64_C(4435)) {
+                                            if (m < INT64_C(2218)) {
+                                                select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
                                                 return out;
                                             } else {
-                                                if (m < INT64_C(555)) {
-                                                    select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
-                                                    return out;
-                                                } else {
-                                                    if (m < INT64_C(1109)) {
-                                                        if (k < INT64_C(144)) {
-                                                            select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
-                                                            return out;
-                                                        } else {
-                                                            select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
-                                                            return out;
-                                                        }
-                                                    } else {
-                                                        select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
-                                                        return out;
-                                                    }
-                                                }
+                                                select_tf32_tn_config out = {1u, 1u, 4u, 8u, 8u};
+                                                return out;
                                             }
-                                        }
-                                    } else {
-                                        if (m < INT64_C(1109)) {
-                                            select_tf32_tn_config out = {2u, 1u, 1u, 16u, 16u};
-                                            return out;
                                         } else {
-                                            select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
-                                            return out;
-                                        }
-                                    }
-                                } else {
-                                    if (m < INT64_C(555)) {
-                                        select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
-                                        return out;
-                                    } else {
-                                        select_tf32_tn_config out = {1u, 1u, 4u, 16u, 16u};
-                                        return out;
-                                    }
-                                }
-                            }
-                        } else {
-                            if (n < INT64_C(1620)) {
-                                if (m < INT64_C(70)) {
-                                    select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
-                                    return out;
-                                } else {
-                                    if (m < INT64_C(448)) {
-                                        if (m < INT64_C(278)) {
-                                            select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
-                                            return out;
-                                        } else {
-                                            if (k < INT64_C(405)) {
+                                            if (m < INT64_C(8870)) {
                                                 select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
                                                 return out;
                                             } else {
-                                                if (k < INT64_C(725)) {
-                                                    select_tf32_tn_config out = {2u, 1u, 1u, 16u, 16u};
+                                                if (n < INT64_C(91)) {
+                                                    select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
                                                     return out;
                                                 } else {
                                                     select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
@@ -435,36 +271,62 @@ static inline select_tf32_tn_config select_tf32_tn(int64_t m, int64_t k, int64_t
                                                 }
                                             }
                                         }
-                                    } else {
-                                        select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
-                                        return out;
                                     }
                                 }
                             } else {
-                                if (k < INT64_C(725)) {
-                                    if (m < INT64_C(139)) {
-                                        select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
-                                        return out;
-                                    } else {
-                                        if (m < INT64_C(278)) {
-                                            select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
+                                select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
+                                return out;
+                            }
+                        }
+                    }
+                } else {
+                    if (k < INT64_C(405)) {
+                        if (m < INT64_C(2218)) {
+                            if (k < INT64_C(111)) {
+                                if (m < INT64_C(1109)) {
+                                    select_tf32_tn_config out = {1u, 1u, 4u, 8u, 8u};
+                                    return out;
+                                } else {
+                                    select_tf32_tn_config out = {8u, 1u, 2u, 8u, 8u};
+                                    return out;
+                                }
+                            } else {
+                                if (n < INT64_C(702)) {
+                                    select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
+                                    return out;
+                                } else {
+                                    if (m < INT64_C(1109)) {
+                                        if (k < INT64_C(227)) {
+                                            select_tf32_tn_config out = {1u, 1u, 4u, 8u, 8u};
                                             return out;
                                         } else {
-                                            select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
+                                            select_tf32_tn_config out = {8u, 1u, 2u, 8u, 8u};
                                             return out;
                                         }
-                                    }
-                                } else {
-                                    if (m < INT64_C(70)) {
-                                        select_tf32_tn_config out = {1u, 1u, 4u, 16u, 16u};
-                                        return out;
                                     } else {
-                                        if (m < INT64_C(139)) {
+                                        select_tf32_tn_config out = {8u, 2u, 4u, 16u, 16u};
+                                        return out;
+                                    }
+                                }
+                            }
+                        } else {
+                            if (k < INT64_C(46)) {
+                                if (m < INT64_C(17740)) {
+                                    if (k < INT64_C(28)) {
+                                        if (m < INT64_C(4435)) {
+                                            select_tf32_tn_config out = {8u, 1u, 2u, 8u, 8u};
+                                            return out;
+                                        } else {
+                                            select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
+                                            return out;
+                                        }
+                                    } else {
+                                        if (m < INT64_C(4435)) {
                                             select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
                                             return out;
                                         } else {
-                                            if (m < INT64_C(393)) {
-                                                select_tf32_tn_config out = {1u, 1u, 4u, 16u, 16u};
+                                            if (m < INT64_C(8870)) {
+                                                select_tf32_tn_config out = {8u, 1u, 2u, 8u, 8u};
                                                 return out;
                                             } else {
                                                 select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
@@ -472,32 +334,298 @@ static inline select_tf32_tn_config select_tf32_tn(int64_t m, int64_t k, int64_t
                                             }
                                         }
                                     }
+                                } else {
+                                    select_tf32_tn_config out = {8u, 1u, 8u, 16u, 16u};
+                                    return out;
+                                }
+                            } else {
+                                if (n < INT64_C(544)) {
+                                    if (m < INT64_C(4435)) {
+                                        select_tf32_tn_config out = {1u, 1u, 4u, 16u, 16u};
+                                        return out;
+                                    } else {
+                                        if (m < INT64_C(17740)) {
+                                            if (k < INT64_C(182)) {
+                                                if (k < INT64_C(91)) {
+                                                    select_tf32_tn_config out = {1u, 1u, 4u, 8u, 8u};
+                                                    return out;
+                                                } else {
+                                                    select_tf32_tn_config out = {8u, 1u, 8u, 16u, 16u};
+                                                    return out;
+                                                }
+                                            } else {
+                                                if (m < INT64_C(8870)) {
+                                                    select_tf32_tn_config out = {1u, 1u, 4u, 8u, 8u};
+                                                    return out;
+                                                } else {
+                                                    select_tf32_tn_config out = {4u, 2u, 8u, 16u, 16u};
+                                                    return out;
+                                                }
+                                            }
+                                        } else {
+                                            select_tf32_tn_config out = {1u, 1u, 4u, 16u, 16u};
+                                            return out;
+                                        }
+                                    }
+                                } else {
+                                    if (k < INT64_C(157)) {
+                                        select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
+                                        return out;
+                                    } else {
+                                        select_tf32_tn_config out = {4u, 2u, 8u, 16u, 16u};
+                                        return out;
+                                    }
                                 }
                             }
                         }
                     } else {
-                        if (k < INT64_C(182)) {
-                            select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
-                            return out;
+                        if (m < INT64_C(1109)) {
+                            if (n < INT64_C(203)) {
+                                select_tf32_tn_config out = {8u, 1u, 2u, 8u, 8u};
+                                return out;
+                            } else {
+                                select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
+                                return out;
+                            }
                         } else {
-                            if (k < INT64_C(363)) {
-                                if (n < INT64_C(725)) {
-                                    select_tf32_tn_config out = {1u, 1u, 4u, 16u, 16u};
+                            if (m < INT64_C(2218)) {
+                                select_tf32_tn_config out = {1u, 1u, 4u, 16u, 16u};
+                                return out;
+                            } else {
+                                if (n < INT64_C(512)) {
+                                    select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
                                     return out;
                                 } else {
-                                    select_tf32_tn_config out = {2u, 1u, 8u, 16u, 16u};
+                                    select_tf32_tn_config out = {4u, 2u, 8u, 16u, 16u};
                                     return out;
                                 }
+                            }
+                        }
+                    }
+                }
+            }
+        } else {
+            if (k < INT64_C(118)) {
+                if (n < INT64_C(118)) {
+                    if (m < INT64_C(567677)) {
+                        select_tf32_tn_config out = {8u, 2u, 4u, 16u, 16u};
+                        return out;
+                    } else {
+                        select_tf32_tn_config out = {4u, 2u, 8u, 16u, 16u};
+                        return out;
+                    }
+                } else {
+                    if (k < INT64_C(40)) {
+                        select_tf32_tn_config out = {4u, 2u, 8u, 16u, 16u};
+                        return out;
+                    } else {
+                        select_tf32_tn_config out = {8u, 1u, 8u, 16u, 16u};
+                        return out;
+                    }
+                }
+            } else {
+                if (n < INT64_C(91)) {
+                    if (k < INT64_C(146)) {
+                        select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
+                        return out;
+                    } else {
+                        if (k < INT64_C(194)) {
+                            if (m < INT64_C(100352)) {
+                                select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
+                                return out;
+                            } else {
+                                select_tf32_tn_config out = {8u, 2u, 4u, 16u, 16u};
+                                return out;
+                            }
+                        } else {
+                            select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
+                            return out;
+                        }
+                    }
+                } else {
+                    select_tf32_tn_config out = {8u, 2u, 4u, 16u, 16u};
+                    return out;
+                }
+            }
+        }
+    } else {
+        if (k < INT64_C(2173)) {
+            if (m < INT64_C(3)) {
+                select_tf32_tn_config out = {1u, 1u, 4u, 8u, 8u};
+                return out;
+            } else {
+                if (m < INT64_C(1792)) {
+                    if (m < INT64_C(1109)) {
+                        if (k < INT64_C(1620)) {
+                            if (n < INT64_C(716)) {
+                                if (m < INT64_C(555)) {
+                                    if (m < INT64_C(70)) {
+                                        select_tf32_tn_config out = {8u, 1u, 2u, 8u, 8u};
+                                        return out;
+                                    } else {
+                                        if (m < INT64_C(278)) {
+                                            select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
+                                            return out;
+                                        } else {
+                                            if (n < INT64_C(363)) {
+                                                select_tf32_tn_config out = {8u, 1u, 2u, 8u, 8u};
+                                                return out;
+                                            } else {
+                                                select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
+                                                return out;
+                                            }
+                                        }
+                                    }
+                                } else {
+                                    select_tf32_tn_config out = {1u, 1u, 4u, 8u, 8u};
+                                    return out;
+                                }
+                            } else {
+                                if (m < INT64_C(393)) {
+                                    if (m < INT64_C(28)) {
+                                        select_tf32_tn_config out = {1u, 1u, 4u, 8u, 8u};
+                                        return out;
+                                    } else {
+                                        if (m < INT64_C(70)) {
+                                            select_tf32_tn_config out = {1u, 1u, 4u, 16u, 16u};
+                                            return out;
+                                        } else {
+                                            select_tf32_tn_config out = {1u, 1u, 4u, 8u, 8u};
+                                            return out;
+                                        }
+                                    }
+                                } else {
+                                    select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
+                                    return out;
+                                }
+                            }
+                        } else {
+                            if (m < INT64_C(12)) {
+                                select_tf32_tn_config out = {1u, 1u, 4u, 16u, 16u};
+                                return out;
+                            } else {
+                                if (m < INT64_C(278)) {
+                                    if (m < INT64_C(40)) {
+                                        select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
+                                        return out;
+                                    } else {
+                                        if (m < INT64_C(139)) {
+                                            select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
+                                            return out;
+                                        } else {
+                                            select_tf32_tn_config out = {1u, 1u, 4u, 8u, 8u};
+                                            return out;
+                                        }
+                                    }
+                                } else {
+                                    select_tf32_tn_config out = {1u, 1u, 4u, 16u, 16u};
+                                    return out;
+                                }
+                            }
+                        }
+                    } else {
+                        select_tf32_tn_config out = {1u, 1u, 4u, 16u, 16u};
+                        return out;
+                    }
+                } else {
+                    if (n < INT64_C(182)) {
+                        if (m < INT64_C(35480)) {
+                            if (m < INT64_C(8870)) {
+                                select_tf32_tn_config out = {1u, 1u, 4u, 8u, 8u};
+                                return out;
+                            } else {
+                                if (m < INT64_C(17740)) {
+                                    select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
+                                    return out;
+                                } else {
+                                    select_tf32_tn_config out = {1u, 1u, 4u, 8u, 8u};
+                                    return out;
+                                }
+                            }
+                        } else {
+                            if (m < INT64_C(70960)) {
+                                select_tf32_tn_config out = {8u, 2u, 4u, 16u, 16u};
+                                return out;
+                            } else {
+                                if (m < INT64_C(141920)) {
+                                    select_tf32_tn_config out = {1u, 1u, 4u, 8u, 8u};
+                                    return out;
+                                } else {
+                                    select_tf32_tn_config out = {8u, 2u, 4u, 16u, 16u};
+                                    return out;
+                                }
+                            }
+                        }
+                    } else {
+                        if (m < INT64_C(2535)) {
+                            select_tf32_tn_config out = {1u, 1u, 4u, 8u, 8u};
+                            return out;
+                        } else {
+                            if (m < INT64_C(8870)) {
+                                select_tf32_tn_config out = {8u, 1u, 8u, 16u, 16u};
+                                return out;
                             } else {
                                 select_tf32_tn_config out = {4u, 2u, 8u, 16u, 16u};
                                 return out;
                             }
                         }
                     }
+                }
+            }
+        } else {
+            if (m < INT64_C(3584)) {
+                if (n < INT64_C(3548)) {
+                    if (m < INT64_C(393)) {
+                        if (m < INT64_C(12)) {
+                            select_tf32_tn_config out = {1u, 1u, 4u, 16u, 16u};
+                            return out;
+                        } else {
+                            if (k < INT64_C(4345)) {
+                                if (m < INT64_C(56)) {
+                                    select_tf32_tn_config out = {1u, 1u, 4u, 8u, 8u};
+                                    return out;
+                                } else {
+                                    select_tf32_tn_config out = {2u, 1u, 1u, 8u, 8u};
+                                    return out;
+                                }
+                            } else {
+                                if (m < INT64_C(139)) {
+                                    select_tf32_tn_config out = {8u, 1u, 2u, 8u, 8u};
+                                    return out;
+                                } else {
+                                    select_tf32_tn_config out = {1u, 1u, 4u, 16u, 16u};
+                                    return out;
+                                }
+                            }
+                        }
+                    } else {
+                        if (n < INT64_C(1255)) {
+                            if (m < INT64_C(1109)) {
+                                if (n < INT64_C(363)) {
+                                    select_tf32_tn_config out = {1u, 1u, 4u, 16u, 16u};
+                                    return out;
+                                } else {
+                                    select_tf32_tn_config out = {8u, 1u, 8u, 16u, 16u};
+                                    return out;
+                                }
+                            } else {
+                                select_tf32_tn_config out = {8u, 1u, 8u, 16u, 16u};
+                                return out;
+                            }
+                        } else {
+                            select_tf32_tn_config out = {4u, 2u, 8u, 16u, 16u};
+                            return out;
+                        }
+                    }
                 } else {
-                    if (m < INT64_C(8870)) {
-                        if (k < INT64_C(182)) {
-                            select_tf32_tn_config out = {8u, 1u, 8u, 8u, 8u};
+                    select_tf32_tn_config out = {8u, 1u, 8u, 16u, 16u};
+                    return out;
+                }
+            } else {
+                if (k < INT64_C(7095)) {
+                    if (n < INT64_C(363)) {
+                        if (m < INT64_C(8870)) {
+                            select_tf32_tn_config out = {8u, 1u, 8u, 16u, 16u};
                             return out;
                         } else {
                             select_tf32_tn_config out = {4u, 2u, 8u, 16u, 16u};
@@ -507,166 +635,8 @@ static inline select_tf32_tn_config select_tf32_tn(int64_t m, int64_t k, int64_t
                         select_tf32_tn_config out = {4u, 2u, 8u, 16u, 16u};
                         return out;
                     }
-                }
-            }
-        } else {
-            if (k < INT64_C(291)) {
-                if (n < INT64_C(23)) {
-                    select_tf32_tn_config out = {2u, 1u, 1u, 16u, 16u};
-                    return out;
                 } else {
-                    select_tf32_tn_config out = {8u, 2u, 4u, 16u, 16u};
-                    return out;
-                }
-            } else {
-                if (n < INT64_C(91)) {
-                    select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
-                    return out;
-                } else {
-                    select_tf32_tn_config out = {8u, 2u, 4u, 16u, 16u};
-                    return out;
-                }
-            }
-        }
-    } else {
-        if (m < INT64_C(1792)) {
-            if (n < INT64_C(2024)) {
-                if (m < INT64_C(555)) {
-                    if (m < INT64_C(6)) {
-                        select_tf32_tn_config out = {1u, 1u, 4u, 16u, 16u};
-                        return out;
-                    } else {
-                        if (m < INT64_C(70)) {
-                            if (k < INT64_C(2897)) {
-                                select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
-                                return out;
-                            } else {
-                                if (m < INT64_C(28)) {
-                                    select_tf32_tn_config out = {1u, 1u, 4u, 16u, 16u};
-                                    return out;
-                                } else {
-                                    select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
-                                    return out;
-                                }
-                            }
-                        } else {
-                            if (m < INT64_C(139)) {
-                                select_tf32_tn_config out = {2u, 1u, 1u, 16u, 16u};
-                                return out;
-                            } else {
-                                if (n < INT64_C(363)) {
-                                    select_tf32_tn_config out = {2u, 1u, 1u, 16u, 16u};
-                                    return out;
-                                } else {
-                                    if (m < INT64_C(278)) {
-                                        if (k < INT64_C(3072)) {
-                                            select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
-                                            return out;
-                                        } else {
-                                            select_tf32_tn_config out = {1u, 1u, 4u, 16u, 16u};
-                                            return out;
-                                        }
-                                    } else {
-                                        select_tf32_tn_config out = {1u, 1u, 4u, 16u, 16u};
-                                        return out;
-                                    }
-                                }
-                            }
-                        }
-                    }
-                } else {
-                    if (m < INT64_C(1109)) {
-                        if (k < INT64_C(2173)) {
-                            select_tf32_tn_config out = {1u, 1u, 4u, 16u, 16u};
-                            return out;
-                        } else {
-                            if (n < INT64_C(363)) {
-                                select_tf32_tn_config out = {1u, 1u, 4u, 16u, 16u};
-                                return out;
-                            } else {
-                                select_tf32_tn_config out = {2u, 1u, 8u, 16u, 16u};
-                                return out;
-                            }
-                        }
-                    } else {
-                        if (n < INT64_C(363)) {
-                            if (k < INT64_C(1630)) {
-                                select_tf32_tn_config out = {2u, 1u, 8u, 16u, 16u};
-                                return out;
-                            } else {
-                                select_tf32_tn_config out = {8u, 1u, 8u, 8u, 8u};
-                                return out;
-                            }
-                        } else {
-                            select_tf32_tn_config out = {2u, 1u, 8u, 16u, 16u};
-                            return out;
-                        }
-                    }
-                }
-            } else {
-                if (m < INT64_C(12)) {
-                    select_tf32_tn_config out = {8u, 1u, 8u, 8u, 8u};
-                    return out;
-                } else {
-                    if (k < INT64_C(10138)) {
-                        select_tf32_tn_config out = {2u, 1u, 8u, 16u, 16u};
-                        return out;
-                    } else {
-                        select_tf32_tn_config out = {8u, 1u, 8u, 8u, 8u};
-                        return out;
-                    }
-                }
-            }
-        } else {
-            if (n < INT64_C(182)) {
-                if (m < INT64_C(35480)) {
-                    if (m < INT64_C(8870)) {
-                        select_tf32_tn_config out = {1u, 1u, 4u, 16u, 16u};
-                        return out;
-                    } else {
-                        select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
-                        return out;
-                    }
-                } else {
-                    select_tf32_tn_config out = {8u, 2u, 4u, 16u, 16u};
-                    return out;
-                }
-            } else {
-                if (m < INT64_C(7168)) {
-                    if (n < INT64_C(363)) {
-                        if (m < INT64_C(4435)) {
-                            if (k < INT64_C(1630)) {
-                                select_tf32_tn_config out = {8u, 1u, 8u, 8u, 8u};
-                                return out;
-                            } else {
-                                select_tf32_tn_config out = {2u, 1u, 8u, 16u, 16u};
-                                return out;
-                            }
-                        } else {
-                            if (k < INT64_C(1630)) {
-                                select_tf32_tn_config out = {2u, 1u, 2u, 8u, 8u};
-                                return out;
-                            } else {
-                                select_tf32_tn_config out = {8u, 1u, 8u, 8u, 8u};
-                                return out;
-                            }
-                        }
-                    } else {
-                        if (m < INT64_C(3584)) {
-                            if (m < INT64_C(3104)) {
-                                select_tf32_tn_config out = {4u, 2u, 8u, 16u, 16u};
-                                return out;
-                            } else {
-                                select_tf32_tn_config out = {8u, 1u, 8u, 8u, 8u};
-                                return out;
-                            }
-                        } else {
-                            select_tf32_tn_config out = {4u, 2u, 8u, 16u, 16u};
-                            return out;
-                        }
-                    }
-                } else {
-                    select_tf32_tn_config out = {4u, 2u, 8u, 16u, 16u};
+                    select_tf32_tn_config out = {1u, 1u, 4u, 8u, 8u};
                     return out;
                 }
             }

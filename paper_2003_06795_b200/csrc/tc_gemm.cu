@@ -1336,9 +1336,67 @@ static kp_status stage_operand(bool bf16, const void* src, int64_t rows, int64_t
     return check_launch("stage_rows_kernel");
 }
 
+// TF32 with both operands MN-major (A transposed, B normal: the TN layout)
+// runs the tensor pipe at ~52 % where any layout with a K-major operand runs
+// at ~66 % (ncu, 4096^3; BF16 TN is unaffected): the 32-byte-granular
+// MN-major swizzle on both sides.  Large TN problems therefore get A copied
+// K-major first (tiled transpose into a stream-ordered temporary, 16-byte
+// row pitch), which costs 2*m*k*4 bytes of traffic against the MMA time it
+// saves; small ones keep the direct path.
+__global__ void __launch_bounds__(256)
+transpose_f32_kernel(const float* __restrict__ src, float* __restrict__ dst, int64_t rows,
+                     int64_t cols, int64_t lds, int64_t ldd) {
+    // src: rows x cols (row pitch lds); dst: cols x rows (row pitch ldd)
+    __shared__ float tile[32][33];
+    const int64_t r0 = int64_t(blockIdx.y) * 32, c0 = int64_t(blockIdx.x) * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8 threads
+#pragma unroll
+    for (int i = 0; i < 32; i += 8) {
+        const int64_t r = r0 + ty + i, c = c0 + tx;
+        tile[ty + i][tx] = (r < rows && c < cols) ? src[r * lds + c] : 0.0f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 32; i += 8) {
+        const int64_t c = c0 + ty + i, r = r0 + tx;
+        if (c < cols && r < rows) dst[c * ldd + r] = tile[tx][ty + i];
+    }
+}
+
+static bool tf32_tn_transpose(kp_family fam, const GemmProblem& g) {
+    static const bool on = [] {
+        const char* e = std::getenv("KP_TC_TN_TRANSPOSE");
+        return !(e && e[0] == '0');
+    }();
+    // measured: 4096^3 291 -> 266 us, 8192^3 1862 -> 1695 us (= the NN
+    // layout's time plus the copy); 2048^3 45 -> 50 us, so large problems only
+    return on && fam == KP_TF32_TC && g.ta && !g.tb && g.batch == 1 && g.m >= 4096 &&
+           g.n >= 4096 && g.k >= 2048;
+}
+
 kp_status launch(kp_family fam, const kp_config& c, const GemmProblem& g, cudaStream_t s) {
     kp_status st = valid(fam, c);
     if (st != KP_OK) return st;
+    if (tf32_tn_transpose(fam, g)) {
+        GemmProblem h = g;
+        h.ta = false;
+        h.lda = (g.k + 3) / 4 * 4;  // A' = op(A) stored m x k, K-major
+        h.sa = 0;
+        void* tmp = nullptr;
+        if (cudaMallocAsync(&tmp, size_t(g.m) * h.lda * 4, s) != cudaSuccess)
+            return check_launch("tc transpose cudaMallocAsync");
+        // A stored k x m (row pitch lda) -> A' m x k
+        const dim3 grid(unsigned((g.m + 31) / 32), unsigned((g.k + 31) / 32));
+        transpose_f32_kernel<<<grid, 256, 0, s>>>(static_cast<const float*>(g.A),
+                                                   static_cast<float*>(tmp), g.k, g.m, g.lda,
+                                                   h.lda);
+        note_launch();
+        st = check_launch("transpose_f32_kernel");
+        h.A = tmp;
+        if (st == KP_OK) st = launch(fam, c, h, s);
+        cudaFreeAsync(tmp, s);
+        return st;
+    }
     const int es = fam == KP_BF16_TC ? 2 : 4;
     auto al = [&](const void* ptr, int64_t ld, int64_t bs) {
         return aligned16(ptr) && (ld * es) % 16 == 0 && (g.batch == 1 || (bs * es) % 16 == 0);
