@@ -347,7 +347,7 @@ def fp32_peaks() -> dict:
 
 def tf32_peak_cublas(dev) -> float:
     """Dense TF32 denominator measured here: cuBLAS (torch.matmul, allow_tf32)
-    on 8192^3 fp32 operands, best of 5 launches (CUDA events), like
+    on 8192^3 fp32 operands, best of 10 launches (CUDA events), like
     MEASURED_PEAKS' bf16 burst figure. MEASURED_PEAKS.json has no TF32 entry."""
     import torch
     prev = torch.backends.cuda.matmul.allow_tf32
@@ -357,11 +357,11 @@ def tf32_peak_cublas(dev) -> float:
         a = torch.randn(n, n, device=dev)
         b = torch.randn(n, n, device=dev)
         c = torch.empty(n, n, device=dev)
-        for _ in range(3):
+        for _ in range(5):
             torch.matmul(a, b, out=c)
         best = float("inf")
         stream = torch.cuda.current_stream()
-        for _ in range(5):
+        for _ in range(10):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             torch.matmul(a, b, out=c)
@@ -380,7 +380,7 @@ def family_peaks(dev) -> dict:
     f32 = fp32_peaks()
     tf32 = tf32_peak_cublas(dev)
     return {"f32": (f32["nominal"], "nominal FP32: " + f32["nominal_how"]),
-            "tf32": (tf32, "cuBLAS TF32 8192^3 measured in this run (burst, best of 5)"),
+            "tf32": (tf32, "cuBLAS TF32 8192^3 measured in this run (burst, best of 10)"),
             "bf16": (mp["bf16_tflops"], mp["source"] + " bf16_tflops (burst)"),
             "_f32": f32, "_hbm_gbs": mp["hbm_gbs"], "_hbm_source": mp["source"]}
 
@@ -783,7 +783,6 @@ def run_gpu(args) -> int:
     # ---- headline family: FP32 SIMT (the paper's 640-config space) ---------
     f32 = FamilyRun("f32", args, dev, rank, world, gloo)
     f32.sweep()
-    peaks = family_peaks(dev)
     clocks = ClockSampler()
     per_size_ms, launches = f32.timed(args.steps, clocks)
     clk = clocks.stop(gpu_index())
@@ -797,35 +796,45 @@ def run_gpu(args) -> int:
     pipe = gemm.PinnedPipeline("f32")
     for _ in range(args.warmup):
         pipe.run(host)
-    f32.barrier()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        pipe.run(host)
-    e2e_s = reduce_over_ranks(time.perf_counter() - t0, world, gloo)
+    # three windows of `steps` steps each (host jitter: pinned-copy and Python
+    # enqueue timing varies between windows); the median window is reported
+    e2e_windows = []
+    for _ in range(3):
+        f32.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            pipe.run(host)
+        e2e_windows.append(reduce_over_ranks(time.perf_counter() - t0, world, gloo))
+    e2e_s = statistics.median(e2e_windows)
     e2e_value = world * args.steps * step_flops / e2e_s / 1e12
 
     # ---- tensor-core families (same workload, their own selectors) -------
-    families = {}
+    families, fam_runs = {}, {}
     fam_steps = max(20, args.steps // 4)
     for fam in ("tf32", "bf16"):
         run = FamilyRun(fam, args, dev, rank, world, gloo)
         run.sweep()
         ms, _ = run.timed(fam_steps)
         tot = reduce_over_ranks(float(ms.sum()), world, gloo)
-        per, pct, dom, mean = run.report(ms)
+        fam_runs[fam] = (run.report(ms), tot, len(run.cells),
+                         len(run.cells) / run.sweep_wall if run.cells else None)
+        del run
+    torch.cuda.empty_cache()
+    # the peak measurements run seconds of full-power GEMMs (cuBLAS TF32, the
+    # FFMA probe): after every timed step, so their power draw cannot lower
+    # the clocks of the timed regions
+    peaks = family_peaks(dev)
+    for fam, ((per, pct, dom, mean), tot, ncells, cps) in fam_runs.items():
         tpk, src = tensor_peak(fam, peaks)
         ach = flops_of(SIZES[dom]) / (mean[dom] * 1e-3) / 1e12
         families[fam] = {
             "value": world * fam_steps * step_flops / (tot * 1e-3) / 1e12, "unit": "TFLOP/s",
             "steps": fam_steps, "pct_oracle_best_in_sample": pct,
-            "sweep": {"cells": len(run.cells), "cells_per_s":
-                      len(run.cells) / run.sweep_wall if run.cells else None},
+            "sweep": {"cells": ncells, "cells_per_s": cps},
             "roofline": {"bound": "tensor", "achieved": ach, "peak": tpk, "unit": "TFLOP/s",
                          "frac": ach / tpk, "peak_source": src,
                          "kernel": f"tc_gemm {per[dom]['config']} @ {SIZES[dom]}^3"},
             "per_size": per, "selector": f"csrc/generated/select_{fam}_nn.h"}
-        del run
-    torch.cuda.empty_cache()
 
     if rank != 0:
         if world > 1:
@@ -880,10 +889,12 @@ def run_gpu(args) -> int:
         "e2e": {"value": e2e_value, "unit": "TFLOP/s",
                 "h2d_bytes_per_step": sum(2 * 4 * s * s for s in SIZES),
                 "d2h_bytes_per_step": sum(4 * s * s for s in SIZES),
+                "windows_tflops": [world * args.steps * step_flops / w / 1e12 for w in e2e_windows],
                 "path": "gemm.PinnedPipeline: pinned H2D (copy stream) + kp_gemm_auto "
                         "(compute stream) + D2H (copy stream), largest problem first, "
                         "2048^3 split into 4 row blocks of A/C so its kernels and D2H run "
-                        "under the remaining H2D; synchronised every step"},
+                        "under the remaining H2D; synchronised every step; median of three "
+                        "windows of `steps` steps"},
         "gpu_launches": launches,
         "clocks": clk,
         "peaks": {"fp32_nominal": fp["nominal"], "fp32_measured": fp["measured"],
