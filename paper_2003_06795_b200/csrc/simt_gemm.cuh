@@ -398,6 +398,96 @@ __device__ __forceinline__ void copy_transpose(uint32_t s, const float* src, int
     }
 }
 
+// Interior copy plan, hoisted out of the K loop (round 2).  The *_full copies
+// above rebuild every pointer, shift and trip count from the kernel
+// parameters at each K slice -- ~220 non-FMA instructions per warp per slice
+// in the selected 2048^3 kernel, issued as one dependent burst right after
+// the barrier.  For a tile whose copies all take the interior path, the
+// per-thread part (first global source, shared offset within a stage, copies
+// per slice) is computed once per tile; a slice is then n copies along two
+// constant strides plus one pointer bump.  Same element -> shared-address
+// mapping as copy_rows_full / copy_direct_full / copy_transpose(full), so
+// the staged tiles (and every result bit) are unchanged.
+struct CopyPlan {
+    const float* gp;  // this thread's first source element at the next slice
+    uint32_t sp;      // byte offset of its first destination within a stage
+    int n;            // copies per slice
+    int64_t gstep;    // global element stride between this thread's copies
+    uint32_t sstep;   // shared byte stride between them
+    int64_t kstep;    // global element advance per K slice
+};
+
+// k-contiguous source (A normal, B transposed kept as rows): copy_rows_full.
+template <int BK>
+__device__ __forceinline__ CopyPlan plan_rows(const float* src, int64_t ld, int log_rows, int tid,
+                                              int log_nthr) {
+    constexpr int RS = Geo<BK>::RS, TPR = BK / 4, LOG_TPR = BK == 32 ? 3 : 2;
+    const int r0 = tid >> LOG_TPR, c0 = (tid & (TPR - 1)) << 2;
+    const int log_dr = log_nthr - LOG_TPR;
+    CopyPlan c;
+    c.n = log_rows >= log_dr ? 1 << (log_rows - log_dr) : int(r0 < (1 << log_rows));
+    c.gp = src + (int64_t)r0 * ld + c0;
+    c.sp = 4u * (r0 * RS + c0);
+    c.gstep = ld << log_dr;
+    c.sstep = (4u * RS) << log_dr;
+    c.kstep = BK;
+    return c;
+}
+
+// K-row source (A transposed, B normal), chunk layout: copy_direct_full's
+// one-column-per-thread case (the caller checks log_nthr >= log_cols - 2).
+template <int BK>
+__device__ __forceinline__ CopyPlan plan_direct(const float* src, int64_t ld, int log_cols, int tid,
+                                                int log_nthr) {
+    const int log_cpr = log_cols - 2;
+    const int log_dr = log_nthr - log_cpr;
+    const int r0 = tid >> log_cpr, c0 = (tid & ((1 << log_cpr) - 1)) << 2;
+    CopyPlan c;
+    c.n = Geo<BK>::LOG_BK >= log_dr ? 1 << (Geo<BK>::LOG_BK - log_dr) : int(r0 < BK);
+    c.gp = src + (int64_t)r0 * ld + c0;
+    c.sp = 4u * chunk_off<BK>(r0, c0);
+    c.gstep = ld << log_dr;
+    c.sstep = 16u << log_dr;
+    c.kstep = (int64_t)BK * ld;
+    return c;
+}
+
+// B transposed, staged transposed (4-byte copies): copy_transpose's
+// fixed-(k, n & 3) case (the caller checks log_rows >= 2, log_nthr >= LOG_BK + 2).
+template <int BK>
+__device__ __forceinline__ CopyPlan plan_transpose(const float* src, int64_t ld, int log_rows,
+                                                   int tid, int log_nthr) {
+    constexpr int LOG_BK = Geo<BK>::LOG_BK;
+    const int nl = tid & 3, k = (tid >> 2) & (BK - 1);
+    const int dn = 1 << (log_nthr - LOG_BK);
+    const int n0 = ((tid >> (LOG_BK + 2)) << 2) + nl;
+    const int rows = 1 << log_rows;
+    CopyPlan c;
+    c.n = n0 < rows ? (rows - n0 + dn - 1) / dn : 0;
+    c.gp = src + (int64_t)n0 * ld + k;
+    c.sp = 4u * chunk_off<BK>(k, n0);
+    c.gstep = (int64_t)dn * ld;
+    c.sstep = 4u * (dn >> 2) * Geo<BK>::CH;
+    c.kstep = BK;
+    return c;
+}
+
+// One slice of a plan into the stage at shared byte address `s`; advances
+// the plan to the next slice.
+template <bool FOUR_BYTE>
+__device__ __forceinline__ void plan_issue(CopyPlan& c, uint32_t s) {
+    const float* gp = c.gp;
+    uint32_t sp = s + c.sp;
+#pragma unroll 2
+    for (int i = 0; i < c.n; ++i) {
+        if constexpr (FOUR_BYTE) cp_async4_full(sp, gp);
+        else cp_async16_full(sp, gp);
+        gp += c.gstep;
+        sp += c.sstep;
+    }
+    c.gp += c.kstep;
+}
+
 // Ordered stream-K hand-off.  A tile split between CTAs c and c+1 is computed
 // k-slices [0, j) by c and [j, KT) by c+1; c writes its raw accumulators into
 // the C tile (beta == 0, so C is scratch until its final write) and publishes
@@ -504,11 +594,48 @@ __global__ void __launch_bounds__(256, KP_SIMT_MIN_BLOCKS) simt_gemm_kernel(cons
         const bool fullA = p.vecA && m0 + bm <= p.M;
         const bool fullB = p.vecB && n0 + bn <= p.N;
 
+        // hoisted interior plans (see CopyPlan), positioned at slice kb.
+        // Thread tiles up to 32 outputs only: the 8x8 tiles already sit at
+        // the 128-register cap, where the plan's ~10 live registers cost more
+        // than the copy arithmetic it removes (profiles/k1_ab/ab_hoist_*.jsonl:
+        // 8x8 NN/NT -4..-9 %, <= 32-output tiles +0..+7 %).
+        constexpr bool HOIST = RT * CT <= 32;
+        const int64_t kb0 = (int64_t)kb << LOG_BK;
+        bool planA_ok = false, planB_ok = false;
+        CopyPlan pa{}, pb{};
+        if constexpr (!HOIST) {
+        } else if constexpr (TA) {
+            planA_ok = fullA && p.log_nthr >= p.log_bm - 2;
+            pa = plan_direct<BK>(A + kb0 * p.lda + m0, p.lda, p.log_bm, tid, p.log_nthr);
+        } else {
+            planA_ok = fullA;
+            pa = plan_rows<BK>(A + (int64_t)m0 * p.lda + kb0, p.lda, p.log_bm, tid, p.log_nthr);
+        }
+        if constexpr (!HOIST) {
+        } else if constexpr (!TB) {
+            planB_ok = fullB && p.log_nthr >= p.log_bn - 2;
+            pb = plan_direct<BK>(B + kb0 * p.ldb + n0, p.ldb, p.log_bn, tid, p.log_nthr);
+        } else if constexpr (BT) {
+            planB_ok = n0 + bn <= p.N && p.log_bn >= 2 && p.log_nthr >= LOG_BK + 2;
+            pb = plan_transpose<BK>(B + (int64_t)n0 * p.ldb + kb0, p.ldb, p.log_bn, tid, p.log_nthr);
+        } else {
+            planB_ok = fullB;
+            pb = plan_rows<BK>(B + (int64_t)n0 * p.ldb + kb0, p.ldb, p.log_bn, tid, p.log_nthr);
+        }
+
         auto issue = [&](int kt, int stage) {
             const int k0 = kt << LOG_BK;
             const uint32_t a_dst = sA_u + 4u * stage * p.a_elems;
             const uint32_t b_dst = sB_u + 4u * stage * p.b_elems;
             const bool kfull = k0 + BK <= p.K;
+            // slices are issued in increasing kt from kb, so the plans'
+            // running pointers sit at kt whenever the interior path is taken
+            // (only the last slice of a ragged K can leave it)
+            if (HOIST && kfull && planA_ok && planB_ok) {
+                plan_issue<false>(pa, a_dst);
+                plan_issue<TB && BT>(pb, b_dst);
+                return;
+            }
             if constexpr (TA) {  // A stored k x m: rows are K
                 const float* src = A + (int64_t)k0 * p.lda + m0;
                 if (fullA && kfull) copy_direct_full<BK>(a_dst, src, p.lda, p.log_bm, tid, p.log_nthr);
