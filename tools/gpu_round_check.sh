@@ -6,8 +6,8 @@
 set -u
 timeout 1200 python -m pytest tests/ -x -q -m gpu 2>&1 | tail -3
 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
-timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
-timeout 600 python bench.py --impl reference --steps 20 > gpurun_out/bench_ref.json 2>&1
+timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/bench.json 2> gpurun_out/bench.err
+timeout 600 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/bench_ref.json 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv \
     --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-sweep \
     --cpu-seconds 1 > gpurun_out/bench_ncu.log 2>&1
